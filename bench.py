@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark: Chung–Lu edges/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+                    [--impl ours|reference] [--mode counter|reference]
+
+One step = one pass of the generator over the whole workload (every source
+node of this rank's UCP partition): the device plan + the sampler with its
+fused fold (streaming configs) or count+scan+write (materialised configs).
+Multi-GPU: launched by torchrun, one process per GPU; each rank generates its
+UCP partition (weak-free strong split of one graph; see `scaling`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CL edges/sec at 1/2/4/8 B200 (n=1e9, avg deg 500); % of HBM-write roofline"
+UNIT = "edges/s"
+BYTES_PER_EDGE = 8  # two uint32 node ids (the algorithmic write per edge)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--n", type=int, default=None, help="override node count (testing only)")
+    ap.add_argument("--mode", default="reference", choices=["reference", "counter"])
+    ap.add_argument("--track-shift", type=int, default=6)
+    ap.add_argument("--ring-log2", type=int, default=28)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- util
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------------- CPU arm
+def cpu_sample_ranges(w: np.ndarray, target_edges: float, k: int):
+    """k disjoint source ranges, spread evenly over [0,n), each with about
+    target_edges expected edges (suffix-form expected degree, cost.cpp:62-77)."""
+    n = w.size
+    S = float(w.sum())
+    suffix = S - np.cumsum(w)  # sum_{v>u} w_v
+    e = w / S * suffix
+    cum = np.cumsum(e)
+    total = cum[-1]
+    ranges = []
+    for i in range(k):
+        start_cost = total * (i + 0.5) / k
+        lo = int(np.searchsorted(cum, start_cost))
+        hi = int(np.searchsorted(cum, cum[min(lo, n - 1)] + target_edges))
+        hi = max(lo + 1, min(hi, n))
+        ranges.append((lo, hi))
+    return ranges
+
+
+def cpu_baseline(w: np.ndarray, seed: int, seconds: float, kind: str = "reference"):
+    """Time the reference CPU generator (oracle/_ref: the unmodified reference
+    library) on a bounded sample of the workload, all host threads in
+    parallel (the acceptance.cpp:221-254 per-partition pattern)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    R = oracle.ref()
+    ws = R.weight_sequence(w)
+    # calibrate: ~0.2 s single-range probe for the per-thread rate
+    probe = cpu_sample_ranges(w, 2e5, 1)
+    tot, ms = R.parallel_ranges_count(ws, ws.sum_S, probe, seed)
+    rate1 = max(tot / max(ms, 1e-3) * 1e3, 1e5)
+    per_thread_edges = rate1 * seconds
+    ranges = cpu_sample_ranges(w, per_thread_edges, cores)
+    tot, ms = R.parallel_ranges_count(ws, ws.sum_S, ranges, seed)
+    del ws
+    return {"value": tot / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{cores} source ranges spread over [0,n), ~{per_thread_edges:.3g} expected "
+                      f"edges each, create_edges_range in parallel std::threads; "
+                      f"{tot} edges in {ms / 1e3:.2f} s"}
+
+
+def run_reference(args):
+    ws_, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1406_1215_b200 import workloads
+    w = workloads.make(args.config, args.n)
+    seed = workloads.WORKLOADS[args.config].seed
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(w, seed + i, args.cpu_seconds / 2)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {workloads.WORKLOADS[args.config].desc}",
+                   "n": int(w.size)},
+        "cpu_baseline": {**r, "value": v},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_1406_1215_b200 import api, runtime, workloads
+
+    wl = workloads.WORKLOADS[args.config]
+    seed = wl.seed
+    t0 = time.time()
+    w_host = runtime.shared_weights(args.config, args.n, world, rank, local)
+    prep_s = time.time() - t0
+    n = int(w_host.size)
+
+    dev = api.Device(local)
+    w_dev = torch.from_numpy(w_host).to(f"cuda:{local}")
+    dev.set_weights(w_dev)
+    del w_dev
+    S = dev.blocked_sum()
+    ws = api.WeightSequence(w_host, S, None, dev)
+    bounds = runtime.plan(ws, world, rank)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+
+    materialise = wl.materialise
+    stream = dev.torch_stream()
+    ring = None
+    out = None
+    if materialise:
+        cap = int(runtime.expected_edges(w_host, S, lo, hi) * 1.01 + 1_000_000)
+        out = torch.empty((cap, 2), dtype=torch.int32, device=f"cuda:{local}")
+    else:
+        ring = torch.empty((1 << args.ring_log2, 2), dtype=torch.int32, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    small_inputs = n * 8 < (256 << 20)
+
+    def step():
+        if materialise:
+            e = api.create_edges_range(ws, S, lo, hi, seed, out=out)
+            return int(e.shape[0])
+        r = api.stream_range(ws, S, lo, hi, seed, mode=args.mode, track_shift=args.track_shift,
+                             degree=deg, accumulate=False, ring=ring)
+        return r.count
+
+    deg = None
+    if not materialise:
+        ntr = (n + (1 << args.track_shift) - 1) >> args.track_shift
+        deg = torch.zeros(ntr, dtype=torch.int32, device=f"cuda:{local}")
+
+    for _ in range(args.warmup):
+        edges = step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = dev.launch_count
+    total_ms, kern_ms, edges_total = 0.0, 0.0, 0
+    for _ in range(args.steps):
+        if small_inputs:
+            flush.zero_()  # L2 flush between timed iterations (inputs < L2)
+            torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        edges = step()
+        ev1.record(stream)
+        ev1.synchronize()
+        total_ms += ev0.elapsed_time(ev1)
+        kern_ms += dev.last_kernel_ms()
+        edges_total += edges
+    launches = dev.launch_count - launches0
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+
+    # max over ranks of the device time; sum of edges
+    ms_step = total_ms / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_step, kern_ms / args.steps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e = torch.tensor([edges_total], dtype=torch.int64, device="cuda")
+        dist.all_reduce(e)
+        ms_step, kern_step = float(t[0]), float(t[1])
+        edges_all = int(e[0]) // args.steps
+    else:
+        kern_step = kern_ms / args.steps
+        edges_all = edges_total // args.steps
+    value = edges_all / (ms_step / 1e3)
+
+    # ---- e2e through the public API with host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = runtime.e2e_measure(args, w_host, world, rank, local, lo, hi, seed, materialise)
+
+    hbm, peak_kind = peaks()
+    my_edges = edges_total // args.steps
+    achieved = my_edges * BYTES_PER_EDGE / (kern_step / 1e3) / 1e9
+    traffic = runtime.ncu_traffic(args.config, args.mode)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(w_host, seed, args.cpu_seconds)
+        except Exception as ex:  # the reference build may be absent on odd boxes
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {wl.desc}", "n": n, "edges_per_step": edges_all,
+                       "stream_mode": args.mode if not materialise else "reference",
+                       "materialised": materialise,
+                       "track_shift": None if materialise else args.track_shift,
+                       "ring_pairs": None if materialise else (1 << args.ring_log2),
+                       "l2": "flushed (256 MB write) between timed steps" if small_inputs
+                       else f"inputs larger than L2 ({n * 8 / 1e9:.1f} GB weights)",
+                       "parallelism": f"ucp{world}", "weights_prep_s": round(prep_s, 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)",
+                         "kernel_ms": kern_step,
+                         "algorithmic_bytes": f"{BYTES_PER_EDGE} B/edge x {my_edges} edges"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

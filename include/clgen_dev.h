@@ -1,0 +1,127 @@
+/*
+ * clgen_dev.h — C ABI of the B200-native Chung–Lu generator.
+ *
+ * This is the drop-in boundary for the reference's generator entry points
+ * (namespace clgen in /root/reference/proj/core).  Plain pointers and sizes
+ * only; no exceptions cross it.  Every function returns CLGEN_OK (0) or a
+ * negative status; clgen_dev_last_error() returns the calling thread's last
+ * message.  The C++ mirror in clgen_b200.hpp turns statuses into
+ * clgen::error exceptions exactly where the reference throws.
+ *
+ * Pointers marked "host or device" are classified with
+ * cudaPointerGetAttributes: device pointers are used in place, host pointers
+ * are staged through the context's device buffers (copies on the context
+ * stream, the call returns when they completed).
+ *
+ * Threading: one context per host thread / GPU (the run_spmd rank analogue,
+ * comm.cpp:204-227).  Contexts share nothing.
+ */
+#ifndef CLGEN_DEV_H
+#define CLGEN_DEV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CLGEN_OK 0
+#define CLGEN_EINVAL (-1)   /* contract violation: the reference throws clgen::error */
+#define CLGEN_ECUDA (-2)    /* CUDA runtime / launch failure */
+#define CLGEN_ENOMEM (-3)   /* device allocation failed */
+#define CLGEN_ERANGE (-4)   /* output capacity exceeded */
+
+typedef struct clgen_dev_ctx clgen_dev_ctx;
+
+/* Stream modes for the sampler. */
+#define CLGEN_STREAM_REFERENCE 0 /* per-node xoshiro256++ (rng.hpp:26-69): bit-exact */
+#define CLGEN_STREAM_COUNTER 1   /* counter-based Philox keyed (seed,u,segment,draw) */
+
+const char* clgen_dev_last_error(void);
+const char* clgen_dev_version(void);
+
+/* Context on CUDA device `device` with its own non-blocking stream. */
+int clgen_dev_create(int device, clgen_dev_ctx** out);
+int clgen_dev_destroy(clgen_dev_ctx* ctx);
+/* The context stream (cudaStream_t) so callers can time / order work on it. */
+void* clgen_dev_stream(clgen_dev_ctx* ctx);
+int clgen_dev_synchronize(clgen_dev_ctx* ctx);
+/* Instrumentation: kernels this context has launched so far, and the device
+ * duration (CUDA events on the context stream) of the last sampler kernel. */
+unsigned long long clgen_dev_launch_count(clgen_dev_ctx* ctx);
+int clgen_dev_last_kernel_ms(clgen_dev_ctx* ctx, float* ms);
+
+/*
+ * Weights: replaces make_weight_sequence(w, SortPolicy::require_sorted)
+ * (weights.cpp:32-55).  `w` (host or device) must be non-increasing and
+ * non-negative; violations return CLGEN_EINVAL with the reference's message
+ * ("weights unsorted at position u").  The context keeps its own device copy.
+ * `n` may be 0.  Node ids must fit uint32 (n <= 2^32).
+ */
+int clgen_dev_set_weights(clgen_dev_ctx* ctx, const double* w, int64_t n);
+int64_t clgen_dev_num_nodes(clgen_dev_ctx* ctx);
+/* Device pointer of the context's weight copy (read-only). */
+const double* clgen_dev_weights(clgen_dev_ctx* ctx);
+
+/*
+ * S = blocked_sum(w) (weights.cpp:21-30): 4096-element blocks folded left to
+ * right from 0.0, partials folded left to right.  Bit-identical.
+ */
+int clgen_dev_blocked_sum(clgen_dev_ctx* ctx, double* S);
+/* blocked_sum(span<const double>) of an arbitrary array (host or device). */
+int clgen_dev_blocked_sum_array(clgen_dev_ctx* ctx, const double* xs, int64_t n, double* S);
+
+/*
+ * Materialised generation: replaces create_edges_range(ws, S, lo, hi, seed,
+ * EdgeVector&) (edge_skip.cpp:60-66, hot loop :20-46).  Writes the edges as
+ * uint32 (u,v) pairs into `pairs` (host or device, 2*cap uint32) in the
+ * reference's emission order (u ascending, then v ascending) and the count to
+ * *count.  Returns CLGEN_ERANGE (with *count set) when count > cap.
+ * *n_flagged = sources whose skip ratio came within 2^-47 of an integer
+ * (where CUDA's and glibc's log/log1p may disagree); their ids are available
+ * from clgen_dev_flagged_nodes.  Errors like the reference for
+ * lo < 0 || hi > n || lo > hi ("create_edges_range: bad node range").
+ */
+int clgen_dev_create_edges_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi,
+                                 uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count,
+                                 int64_t* n_flagged);
+
+/*
+ * Replaces create_edges(ws, S, sources, seed, sink) (edge_skip.cpp:50-58):
+ * the sources (host or device int64, k entries) are walked in list order and
+ * their edges written in that order.  Any source outside [0,n) returns
+ * CLGEN_EINVAL ("create_edges: source node out of range").
+ */
+int clgen_dev_create_edges(clgen_dev_ctx* ctx, double S, const int64_t* sources, int64_t k,
+                           uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count,
+                           int64_t* n_flagged);
+
+/* Count pass only: per-source edge counts (int32, hi-lo entries, host or device). */
+int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,
+                          int32_t* counts, int64_t* total, int64_t* n_flagged);
+
+/*
+ * Streaming generation with fused fold (no materialised edge list):
+ * *count = edges, *checksum = sum over edges of mix64((u<<32)|v) mod 2^64
+ * (rng.hpp:11-16 finaliser), `degree` (host or device, may be NULL) receives
+ * undirected degrees of the tracked nodes x with x % 2^track_shift == 0 at
+ * degree[x >> track_shift] (uint32, ceil(n / 2^track_shift) entries; counts
+ * are ADDED to the existing contents when `degree` is a device pointer and
+ * `accumulate` != 0, else overwritten).  When `ring` (device) is non-NULL
+ * every edge is also written into it at (position mod ring_cap); ring_cap is
+ * a power of two.  stream_mode selects CLGEN_STREAM_REFERENCE (bit-exact
+ * per-node streams) or CLGEN_STREAM_COUNTER.
+ */
+int clgen_dev_stream_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,
+                           int stream_mode, int track_shift, uint32_t* degree, int accumulate,
+                           uint32_t* ring, int64_t ring_cap, int64_t* count, uint64_t* checksum,
+                           int64_t* n_flagged);
+
+/* Ids of the sources flagged by the last generation call (up to cap). */
+int clgen_dev_flagged_nodes(clgen_dev_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CLGEN_DEV_H */

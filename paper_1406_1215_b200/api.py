@@ -1,0 +1,317 @@
+"""Python mirror of the reference generator API (namespace clgen), backed by
+the sm_100a library through the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/clgen/{weights,edge_skip}.hpp so parity
+tests read like the reference's own tests:
+
+=========================  ==================================================
+this module                reference
+=========================  ==================================================
+``WeightSequence``         ``WeightSequence`` (weights.hpp:14-20)
+``make_weight_sequence``   ``make_weight_sequence`` (weights.cpp:32-55)
+``blocked_sum``            ``blocked_sum`` (weights.cpp:21-30)
+``create_edges_range``     ``create_edges_range`` (edge_skip.cpp:60-66)
+``create_edges``           ``create_edges`` (edge_skip.cpp:50-58)
+``serial_cl``              ``serial_cl`` (edge_skip.cpp:68-70)
+``stream_range``           streaming fold (no reference counterpart; the
+                           count-only ``EdgeCounter`` sink generalised)
+=========================  ==================================================
+
+Edges are returned as ``uint32[m, 2]`` (u, v) pairs — the device layout; the
+reference's ``Edge`` is two int64 (edge_skip.hpp:15-18), widen with
+``.astype(np.int64)`` when comparing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _lib
+from ._lib import STREAM_COUNTER, STREAM_REFERENCE, check, error
+
+try:  # torch is plumbing only: device buffers and streams
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+class SortPolicy(Enum):
+    require_sorted = 0
+    sort_desc = 1
+
+
+def _addr(x) -> int:
+    """Raw pointer of a numpy array or torch tensor (host or device)."""
+    if x is None:
+        return 0
+    if torch is not None and isinstance(x, torch.Tensor):
+        if not x.is_contiguous():
+            raise error("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise error("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(x)!r}")
+
+
+class Device:
+    """One ``clgen_dev_ctx``: a CUDA device, its stream and resident weights."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        check(L.clgen_dev_create(int(device), C.byref(h)))
+        self._h = h
+        self.index = int(device)
+        self._stream = None
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.lib().clgen_dev_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream_ptr(self) -> int:
+        return _lib.lib().clgen_dev_stream(self._h)
+
+    def torch_stream(self):
+        """The context stream as a torch stream (for CUDA-event timing)."""
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.stream_ptr, device=f"cuda:{self.index}")
+        return self._stream
+
+    def synchronize(self) -> None:
+        check(_lib.lib().clgen_dev_synchronize(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        """Kernels launched by this context so far."""
+        return int(_lib.lib().clgen_dev_launch_count(self._h))
+
+    def last_kernel_ms(self) -> float:
+        """Device time of the last sampler kernel (CUDA events on the context stream)."""
+        ms = C.c_float()
+        check(_lib.lib().clgen_dev_last_kernel_ms(self._h, C.byref(ms)))
+        return ms.value
+
+    def set_weights(self, w) -> None:
+        if isinstance(w, np.ndarray):
+            w = np.ascontiguousarray(w, np.float64)
+        elif torch is not None and isinstance(w, torch.Tensor):
+            if w.dtype != torch.float64:
+                raise error("weights must be float64")
+            w = w.contiguous()
+        n = int(w.shape[0]) if w is not None else 0
+        check(_lib.lib().clgen_dev_set_weights(self._h, _addr(w) if n else None, n))
+
+    @property
+    def n(self) -> int:
+        return int(_lib.lib().clgen_dev_num_nodes(self._h))
+
+    def weights_tensor(self):
+        """Zero-copy torch view of the resident weights (float64, device)."""
+        ptr = _lib.lib().clgen_dev_weights(self._h)
+        n = self.n
+        if n == 0:
+            return torch.empty(0, dtype=torch.float64, device=f"cuda:{self.index}")
+        return _device_view(ptr, n, torch.float64, self.index)
+
+    def blocked_sum(self) -> float:
+        out = C.c_double()
+        check(_lib.lib().clgen_dev_blocked_sum(self._h, C.byref(out)))
+        return out.value
+
+    def flagged_nodes(self) -> np.ndarray:
+        n = C.c_int64()
+        buf = np.empty(4096, np.int64)
+        check(_lib.lib().clgen_dev_flagged_nodes(self._h, buf.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                 buf.size, C.byref(n)))
+        return buf[: min(n.value, buf.size)]
+
+
+def _device_view(ptr: int, n: int, dtype, device: int):
+    """Wrap a raw device pointer owned by the library as a torch tensor (no copy)."""
+    itemsize = torch.empty((), dtype=dtype).element_size()
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n,),
+            "typestr": {torch.float64: "<f8", torch.int64: "<i8", torch.uint32: "<u4"}[dtype],
+            "data": (ptr, True),
+            "version": 3,
+        }
+
+    del itemsize
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Holder(), device=f"cuda:{device}")
+
+
+_default_devices: dict[int, Device] = {}
+
+
+def default_device(index: int = 0) -> Device:
+    if index not in _default_devices:
+        _default_devices[index] = Device(index)
+    return _default_devices[index]
+
+
+@dataclass
+class WeightSequence:
+    """Sorted non-increasing weights resident on one GPU (weights.hpp:14-20).
+
+    ``weights`` is the host copy (float64), ``sum_S`` the canonical
+    ``blocked_sum`` computed on the device, ``orig_labels`` the permutation
+    back to input order.  ``device`` owns the device copy.
+    """
+
+    weights: np.ndarray
+    sum_S: float
+    orig_labels: np.ndarray
+    device: Device = field(repr=False)
+
+    def size(self) -> int:
+        return int(self.weights.shape[0])
+
+    @property
+    def n(self) -> int:
+        return self.size()
+
+
+def make_weight_sequence(weights, policy: SortPolicy = SortPolicy.require_sorted,
+                         device: Device | int | None = None) -> WeightSequence:
+    """weights.cpp:32-55.  ``sort_desc`` is a stable descending sort with labels;
+    ``require_sorted`` raises ``error("weights unsorted at position u")``."""
+    # each sequence owns its context unless one is passed in explicitly
+    dev = device if isinstance(device, Device) else Device(device or 0)
+    w = np.ascontiguousarray(weights, np.float64).reshape(-1)
+    labels = np.arange(w.size, dtype=np.int64)
+    if policy == SortPolicy.sort_desc:
+        labels = np.argsort(-w, kind="stable").astype(np.int64)
+        w = np.ascontiguousarray(w[labels])
+    dev.set_weights(w)  # validates order on the device
+    S = dev.blocked_sum()
+    return WeightSequence(w, S, labels, dev)
+
+
+def blocked_sum(xs, device: Device | int | None = None) -> float:
+    """weights.cpp:21-30 on the device, for any sequence (host or device)."""
+    dev = device if isinstance(device, Device) else default_device(device or 0)
+    if isinstance(xs, np.ndarray) or not (torch is not None and isinstance(xs, torch.Tensor)):
+        xs = np.ascontiguousarray(xs, np.float64).reshape(-1)
+    out = C.c_double()
+    n = int(xs.shape[0])
+    check(_lib.lib().clgen_dev_blocked_sum_array(dev.handle, _addr(xs) if n else None, n,
+                                                 C.byref(out)))
+    return out.value
+
+
+def _as_pairs(buf: np.ndarray, m: int) -> np.ndarray:
+    return buf[:m]
+
+
+def create_edges_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
+                       out=None, return_flagged: bool = False):
+    """edge_skip.cpp:60-66.  Returns ``uint32[m,2]`` (host) or fills ``out``
+    (a device tensor of shape [cap,2], uint32/int32) and returns its prefix."""
+    L = _lib.lib()
+    cnt, nfl = C.c_int64(), C.c_int64()
+    if out is None:
+        # size with the count pass (cheap relative to materialisation)
+        total = edge_total(ws, S, lo, hi, seed)
+        buf = np.empty((max(total, 1), 2), np.uint32)
+        check(L.clgen_dev_create_edges_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF,
+                                             buf.ctypes.data, total, C.byref(cnt), C.byref(nfl)))
+        res = buf[: cnt.value]
+    else:
+        cap = int(out.shape[0])
+        rc = L.clgen_dev_create_edges_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF,
+                                            _addr(out), cap, C.byref(cnt), C.byref(nfl))
+        check(rc)
+        res = out[: cnt.value]
+    return (res, nfl.value) if return_flagged else res
+
+
+def create_edges(ws: WeightSequence, S: float, sources, seed: int, return_flagged: bool = False):
+    """edge_skip.cpp:50-58: sources walked in list order."""
+    L = _lib.lib()
+    src = np.ascontiguousarray(sources, np.int64).reshape(-1)
+    cnt, nfl = C.c_int64(), C.c_int64()
+    # first call with cap=0 learns the count (CLGEN_ERANGE when non-zero)
+    rc = L.clgen_dev_create_edges(ws.device.handle, S, src.ctypes.data if src.size else None,
+                                  src.size, seed & 0xFFFFFFFFFFFFFFFF, None, 0, C.byref(cnt),
+                                  C.byref(nfl))
+    if rc not in (_lib.CLGEN_OK, _lib.CLGEN_ERANGE):
+        check(rc)
+    total = cnt.value
+    buf = np.empty((max(total, 1), 2), np.uint32)
+    if total:
+        check(L.clgen_dev_create_edges(ws.device.handle, S, src.ctypes.data, src.size,
+                                       seed & 0xFFFFFFFFFFFFFFFF, buf.ctypes.data, total,
+                                       C.byref(cnt), C.byref(nfl)))
+    res = buf[: cnt.value]
+    return (res, nfl.value) if return_flagged else res
+
+
+def serial_cl(ws: WeightSequence, seed: int, return_flagged: bool = False):
+    """edge_skip.cpp:68-70."""
+    return create_edges_range(ws, ws.sum_S, 0, ws.size(), seed, return_flagged=return_flagged)
+
+
+def edge_counts(ws: WeightSequence, S: float, lo: int, hi: int, seed: int) -> np.ndarray:
+    """Count pass: per-source edge counts for [lo, hi)."""
+    out = np.empty(max(hi - lo, 1), np.int32)
+    tot, nfl = C.c_int64(), C.c_int64()
+    check(_lib.lib().clgen_dev_edge_counts(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF,
+                                           out.ctypes.data, C.byref(tot), C.byref(nfl)))
+    return out[: hi - lo]
+
+
+def edge_total(ws: WeightSequence, S: float, lo: int, hi: int, seed: int) -> int:
+    tot, nfl = C.c_int64(), C.c_int64()
+    check(_lib.lib().clgen_dev_edge_counts(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF,
+                                           None, C.byref(tot), C.byref(nfl)))
+    return tot.value
+
+
+@dataclass
+class StreamResult:
+    count: int
+    checksum: int
+    flagged: int
+    degree: object = None  # uint32 tracked degrees (numpy or the caller's tensor)
+
+
+def stream_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
+                 mode: str = "reference", track_shift: int | None = None, degree=None,
+                 accumulate: bool = False, ring=None) -> StreamResult:
+    """Streaming generation fused with the fold (edge count, 64-bit checksum
+    sum mix64((u<<32)|v), tracked undirected degrees).  ``track_shift=None``
+    disables degree tracking.  ``ring`` (device uint32 tensor [cap,2], cap a
+    power of two) receives every edge at position mod cap."""
+    L = _lib.lib()
+    sm = {"reference": STREAM_REFERENCE, "counter": STREAM_COUNTER}[mode]
+    cnt, cks, nfl = C.c_int64(), C.c_uint64(), C.c_int64()
+    if track_shift is not None and degree is None:
+        ntr = (ws.size() + (1 << track_shift) - 1) >> track_shift
+        degree = np.zeros(max(ntr, 1), np.uint32)
+    ring_cap = int(ring.shape[0]) if ring is not None else 0
+    check(L.clgen_dev_stream_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF, sm,
+                                   track_shift or 0, _addr(degree) if degree is not None else None,
+                                   int(accumulate), _addr(ring) if ring is not None else None,
+                                   ring_cap, C.byref(cnt), C.byref(cks), C.byref(nfl)))
+    return StreamResult(cnt.value, cks.value, nfl.value, degree)

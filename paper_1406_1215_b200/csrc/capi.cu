@@ -1,0 +1,523 @@
+// C ABI of the B200 Chung–Lu generator (include/clgen_dev.h).
+//
+// Host orchestration of the device pipeline.  Each entry point validates its
+// contract exactly where the reference throws clgen::error, launches the
+// sm_100a kernels on the context stream, and synchronises only when a scalar
+// result must be returned to the caller.
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/clgen_dev.h"
+#include "common.cuh"
+#include "sampler_ref.cuh"
+#include "scan.cuh"
+#include "weights.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(CLGEN_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),    \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// Growable device scratch buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Small per-call device scalars (one allocation, zeroed per call).
+struct Scalars {
+  unsigned long long queue;
+  unsigned long long ticket;
+  unsigned long long flag_count;
+  unsigned long long overflow;
+  unsigned long long fold[2];
+  unsigned long long ring_head;
+  unsigned long long first_bad;
+  unsigned long long first_negative;
+  int64_t total;
+  double S;
+};
+
+constexpr int64_t kFlagCap = 4096;
+
+}  // namespace
+
+struct clgen_dev_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  double* w = nullptr;
+  int64_t n = 0;
+  size_t w_bytes = 0;
+  Scalars* sc = nullptr;     // device
+  Scalars* sc_host = nullptr;  // pinned mirror
+  int64_t* flagged = nullptr;  // device, kFlagCap
+  int64_t last_flagged = 0;
+  DevBuf counts, offsets, tiles, pairs, partials, degree, sources;
+  int walk_blocks[3] = {0, 0, 0};
+  // instrumentation: kernels launched by this context, and the duration of
+  // the last dominant (sampler) kernel measured with events on the stream
+  unsigned long long launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+};
+
+namespace {
+
+int set_device(clgen_dev_ctx* c) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  return CLGEN_OK;
+}
+
+int reset_scalars(clgen_dev_ctx* c, unsigned long long queue_start) {
+  Scalars z;
+  std::memset(&z, 0, sizeof z);
+  z.queue = queue_start;
+  z.first_bad = ~0ull;
+  z.first_negative = ~0ull;
+  *c->sc_host = z;
+  CUDA_TRY(cudaMemcpyAsync(c->sc, c->sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
+  return CLGEN_OK;
+}
+
+int fetch_scalars(clgen_dev_ctx* c) {
+  CUDA_TRY(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
+template <int MODE>
+int walk_grid(clgen_dev_ctx* c) {
+  if (!c->walk_blocks[MODE]) {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ref_walk_kernel<MODE>, 256, 0));
+    c->walk_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+  }
+  return c->walk_blocks[MODE];
+}
+
+template <int MODE>
+int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a) {
+  const int grid = walk_grid<MODE>(c);
+  if (grid < 0) return grid;
+  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+  clg::ref_walk_kernel<MODE><<<grid, 256, 0, c->stream>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  c->timed = true;
+  ++c->launches;
+  return CLGEN_OK;
+}
+
+clg::RefWalkArgs walk_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed) {
+  clg::RefWalkArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.w = c->w;
+  a.n = c->n;
+  a.S = S;
+  a.lo = lo;
+  a.hi = hi;
+  a.seed = seed;
+  a.queue = &c->sc->queue;
+  a.flag_count = &c->sc->flag_count;
+  a.flagged = c->flagged;
+  a.flag_cap = kFlagCap;
+  a.overflow = &c->sc->overflow;
+  a.fold_out = c->sc->fold;
+  a.ring_head = &c->sc->ring_head;
+  return a;
+}
+
+int check_range(clgen_dev_ctx* c, int64_t lo, int64_t hi) {
+  if (lo < 0 || hi > c->n || lo > hi) return fail(CLGEN_EINVAL, "create_edges_range: bad node range");
+  return CLGEN_OK;
+}
+
+// counts[0..m) -> offsets[0..m) exclusive, total in sc->total.
+int launch_scan(clgen_dev_ctx* c, const int32_t* counts, int64_t* offsets, int64_t m) {
+  const int64_t ntiles = (m + clg::kScanTile - 1) / clg::kScanTile;
+  if (ntiles == 0) {
+    CUDA_TRY(cudaMemsetAsync(&c->sc->total, 0, sizeof(int64_t), c->stream));
+    return CLGEN_OK;
+  }
+  CUDA_TRY(c->tiles.ensure(ntiles * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(c->tiles.p, 0, ntiles * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(cudaMemsetAsync(&c->sc->ticket, 0, sizeof(unsigned long long), c->stream));
+  clg::scan_lookback_kernel<int32_t><<<static_cast<unsigned>(ntiles), clg::kScanThreads, 0, c->stream>>>(
+      counts, offsets, m, c->tiles.as<unsigned long long>(), &c->sc->ticket, &c->sc->total, 0);
+  CUDA_TRY(cudaGetLastError());
+  ++c->launches;
+  return CLGEN_OK;
+}
+
+// weights.cpp:21-30 on device data d[0..n).
+int blocked_sum_impl(clgen_dev_ctx* c, const double* d, int64_t n, double* S) {
+  int rc = set_device(c);
+  if (rc) return rc;
+  if (n == 0) {
+    *S = 0.0;
+    return CLGEN_OK;
+  }
+  const int64_t nblocks = (n + clg::kSumBlock - 1) / clg::kSumBlock;
+  CUDA_TRY(c->partials.ensure(nblocks * sizeof(double)));
+  const unsigned grid = static_cast<unsigned>((nblocks + 127) / 128);
+  clg::blocked_partials_kernel<<<grid, 128, 0, c->stream>>>(d, n, c->partials.as<double>(), nblocks);
+  CUDA_TRY(cudaGetLastError());
+  clg::fold_partials_kernel<<<1, 32, 0, c->stream>>>(c->partials.as<double>(), nblocks, &c->sc->S);
+  CUDA_TRY(cudaGetLastError());
+  c->launches += 2;
+  if ((rc = fetch_scalars(c))) return rc;
+  *S = c->sc_host->S;
+  return CLGEN_OK;
+}
+
+// Two-pass materialisation in the reference's emission order: count pass,
+// decoupled-lookback scan of the per-slot counts, replay pass writing each
+// slot's edges at its scanned offset.
+int materialise(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, const int64_t* d_sources,
+                uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count, int64_t* n_flagged) {
+  if (cap < 0 || (cap > 0 && !pairs)) return fail(CLGEN_EINVAL, "create_edges: bad output buffer");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t m = hi - lo;
+  if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
+  if (m == 0) {
+    if (count) *count = 0;
+    if (n_flagged) *n_flagged = 0;
+    c->last_flagged = 0;
+    return CLGEN_OK;
+  }
+  CUDA_TRY(c->counts.ensure(m * sizeof(int32_t)));
+  CUDA_TRY(c->offsets.ensure(m * sizeof(int64_t)));
+  clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+  a.sources = d_sources;
+  a.counts = c->counts.as<int32_t>();
+  if ((rc = launch_walk<clg::kWalkCount>(c, a))) return rc;
+  if ((rc = launch_scan(c, a.counts, c->offsets.as<int64_t>(), m))) return rc;
+  const bool dev_out = is_device_ptr(pairs);
+  uint2* d_pairs = reinterpret_cast<uint2*>(pairs);
+  if (!dev_out) {
+    // host output: the exact count sizes the staging buffer
+    if ((rc = fetch_scalars(c))) return rc;
+    const int64_t total = c->sc_host->total;
+    const int64_t stage = total < cap ? total : cap;
+    CUDA_TRY(c->pairs.ensure((stage > 0 ? stage : 1) * sizeof(uint2)));
+    d_pairs = c->pairs.as<uint2>();
+    cap = stage;
+  }
+  c->sc_host->queue = static_cast<unsigned long long>(lo);
+  CUDA_TRY(cudaMemcpyAsync(&c->sc->queue, &c->sc_host->queue, sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemsetAsync(&c->sc->flag_count, 0, sizeof(unsigned long long), c->stream));
+  a.counts = nullptr;
+  a.offsets = c->offsets.as<int64_t>();
+  a.pairs = d_pairs;
+  a.cap = cap;
+  if ((rc = launch_walk<clg::kWalkWrite>(c, a))) return rc;
+  if (!dev_out && cap > 0)
+    CUDA_TRY(cudaMemcpyAsync(pairs, d_pairs, cap * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  const int64_t total = c->sc_host->total;
+  if (count) *count = total;
+  c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);
+  if (n_flagged) *n_flagged = c->last_flagged;
+  if (total > cap)
+    return fail(CLGEN_ERANGE, "create_edges: %lld edges exceed capacity %lld", (long long)total, (long long)cap);
+  return CLGEN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* clgen_dev_last_error(void) { return g_err.c_str(); }
+
+const char* clgen_dev_version(void) { return "clgen-b200 0.1 (sm_100a)"; }
+
+int clgen_dev_create(int device, clgen_dev_ctx** out) {
+  if (!out) return fail(CLGEN_EINVAL, "clgen_dev_create: null out");
+  *out = nullptr;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CLGEN_EINVAL, "clgen_dev_create: no CUDA device %d", device);
+  auto* c = new clgen_dev_ctx;
+  c->device = device;
+  int rc = set_device(c);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&c->sc, sizeof(Scalars)) != cudaSuccess ||
+      cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
+      cudaMalloc(&c->flagged, kFlagCap * sizeof(int64_t)) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    clgen_dev_destroy(c);
+    return fail(CLGEN_ENOMEM, "clgen_dev_create: allocation failed");
+  }
+  *out = c;
+  return CLGEN_OK;
+}
+
+int clgen_dev_destroy(clgen_dev_ctx* c) {
+  if (!c) return CLGEN_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->w) cudaFree(c->w);
+  if (c->sc) cudaFree(c->sc);
+  if (c->sc_host) cudaFreeHost(c->sc_host);
+  if (c->flagged) cudaFree(c->flagged);
+  c->counts.release();
+  c->offsets.release();
+  c->tiles.release();
+  c->pairs.release();
+  c->partials.release();
+  c->degree.release();
+  c->sources.release();
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return CLGEN_OK;
+}
+
+void* clgen_dev_stream(clgen_dev_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+unsigned long long clgen_dev_launch_count(clgen_dev_ctx* c) { return c ? c->launches : 0ull; }
+
+int clgen_dev_last_kernel_ms(clgen_dev_ctx* c, float* ms) {
+  if (!c || !ms) return fail(CLGEN_EINVAL, "last_kernel_ms: null argument");
+  if (!c->timed) return fail(CLGEN_EINVAL, "last_kernel_ms: no sampler kernel launched yet");
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  CUDA_TRY(cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return CLGEN_OK;
+}
+
+int clgen_dev_synchronize(clgen_dev_ctx* c) {
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
+int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (n < 0) return fail(CLGEN_EINVAL, "set_weights: negative n");
+  if (n > (int64_t(1) << 32)) return fail(CLGEN_EINVAL, "set_weights: n exceeds uint32 node ids");
+  if (n > 0 && !w) return fail(CLGEN_EINVAL, "set_weights: null weights");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  if (bytes > c->w_bytes) {
+    if (c->w) cudaFree(c->w);
+    c->w = nullptr;
+    c->w_bytes = 0;
+    if (cudaMalloc(&c->w, bytes ? bytes : 8) != cudaSuccess)
+      return fail(CLGEN_ENOMEM, "set_weights: cannot allocate %lld weights", (long long)n);
+    c->w_bytes = bytes;
+  }
+  c->n = 0;
+  if (n > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->w, w, bytes, cudaMemcpyDefault, c->stream));
+    rc = reset_scalars(c, 0);
+    if (rc) return rc;
+    const int grid = c->num_sms * 8;
+    clg::check_sorted_kernel<<<grid, 256, 0, c->stream>>>(c->w, n, &c->sc->first_bad, &c->sc->first_negative);
+    CUDA_TRY(cudaGetLastError());
+    ++c->launches;
+    rc = fetch_scalars(c);
+    if (rc) return rc;
+    if (c->sc_host->first_negative != ~0ull)
+      return fail(CLGEN_EINVAL, "weights negative or NaN at position %llu", c->sc_host->first_negative);
+    if (c->sc_host->first_bad != ~0ull)
+      return fail(CLGEN_EINVAL, "weights unsorted at position %llu", c->sc_host->first_bad);
+  }
+  c->n = n;
+  return CLGEN_OK;
+}
+
+int64_t clgen_dev_num_nodes(clgen_dev_ctx* c) { return c ? c->n : -1; }
+
+const double* clgen_dev_weights(clgen_dev_ctx* c) { return c ? c->w : nullptr; }
+
+int clgen_dev_blocked_sum(clgen_dev_ctx* c, double* S) {
+  if (!c || !S) return fail(CLGEN_EINVAL, "blocked_sum: null argument");
+  return blocked_sum_impl(c, c->w, c->n, S);
+}
+
+int clgen_dev_blocked_sum_array(clgen_dev_ctx* c, const double* xs, int64_t n, double* S) {
+  if (!c || !S || n < 0 || (n > 0 && !xs)) return fail(CLGEN_EINVAL, "blocked_sum: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const double* d = xs;
+  if (n > 0 && !is_device_ptr(xs)) {
+    CUDA_TRY(c->sources.ensure(n * sizeof(double)));
+    CUDA_TRY(cudaMemcpyAsync(c->sources.p, xs, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    d = c->sources.as<double>();
+  }
+  return blocked_sum_impl(c, d, n, S);
+}
+
+int clgen_dev_edge_counts(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed,
+                          int32_t* counts, int64_t* total, int64_t* n_flagged) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  int rc = check_range(c, lo, hi);
+  if (rc) return rc;
+  if ((rc = set_device(c))) return rc;
+  const int64_t m = hi - lo;
+  const bool dev_out = is_device_ptr(counts);
+  CUDA_TRY(c->counts.ensure((m > 0 ? m : 1) * sizeof(int32_t)));
+  int32_t* d_counts = dev_out ? counts : c->counts.as<int32_t>();
+  if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
+  if (m > 0) {
+    clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+    a.counts = d_counts;
+    if ((rc = launch_walk<clg::kWalkCount>(c, a))) return rc;
+    CUDA_TRY(c->offsets.ensure(m * sizeof(int64_t)));
+    if ((rc = launch_scan(c, d_counts, c->offsets.as<int64_t>(), m))) return rc;
+  }
+  if (counts && !dev_out && m > 0)
+    CUDA_TRY(cudaMemcpyAsync(counts, d_counts, m * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  if (total) *total = m > 0 ? c->sc_host->total : 0;
+  c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);
+  if (n_flagged) *n_flagged = c->last_flagged;
+  return CLGEN_OK;
+}
+
+int clgen_dev_create_edges_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed,
+                                 uint32_t* pairs, int64_t cap, int64_t* count, int64_t* n_flagged) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  int rc = check_range(c, lo, hi);
+  if (rc) return rc;
+  return materialise(c, S, lo, hi, nullptr, seed, pairs, cap, count, n_flagged);
+}
+
+int clgen_dev_create_edges(clgen_dev_ctx* c, double S, const int64_t* sources, int64_t k,
+                           uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count,
+                           int64_t* n_flagged) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (k < 0 || (k > 0 && !sources)) return fail(CLGEN_EINVAL, "create_edges: bad source list");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t* d_src = sources;
+  if (k > 0 && !is_device_ptr(sources)) {
+    CUDA_TRY(c->sources.ensure(k * sizeof(int64_t)));
+    CUDA_TRY(cudaMemcpyAsync(c->sources.p, sources, k * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    d_src = c->sources.as<int64_t>();
+  }
+  if (k > 0) {
+    if ((rc = reset_scalars(c, 0))) return rc;
+    clg::check_sources_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(d_src, k, c->n, &c->sc->first_bad);
+    CUDA_TRY(cudaGetLastError());
+    ++c->launches;
+    if ((rc = fetch_scalars(c))) return rc;
+    if (c->sc_host->first_bad != ~0ull) return fail(CLGEN_EINVAL, "create_edges: source node out of range");
+  }
+  return materialise(c, S, 0, k, d_src, seed, pairs, cap, count, n_flagged);
+}
+
+int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed,
+                           int stream_mode, int track_shift, uint32_t* degree, int accumulate,
+                           uint32_t* ring, int64_t ring_cap, int64_t* count, uint64_t* checksum,
+                           int64_t* n_flagged) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  int rc = check_range(c, lo, hi);
+  if (rc) return rc;
+  if (track_shift < 0 || track_shift > 40) return fail(CLGEN_EINVAL, "stream_range: bad track_shift");
+  if (ring && (ring_cap <= 0 || (ring_cap & (ring_cap - 1)) != 0))
+    return fail(CLGEN_EINVAL, "stream_range: ring_cap must be a power of two");
+  if (ring && !is_device_ptr(ring)) return fail(CLGEN_EINVAL, "stream_range: ring must be device memory");
+  if (stream_mode != CLGEN_STREAM_REFERENCE)
+    return fail(CLGEN_EINVAL, "stream_range: unknown stream mode %d", stream_mode);
+  if ((rc = set_device(c))) return rc;
+  const int64_t ntracked = (c->n + (int64_t(1) << track_shift) - 1) >> track_shift;
+  const bool dev_deg = is_device_ptr(degree);
+  uint32_t* d_deg = degree;
+  if (degree && !dev_deg) {
+    CUDA_TRY(c->degree.ensure((ntracked > 0 ? ntracked : 1) * sizeof(uint32_t)));
+    d_deg = c->degree.as<uint32_t>();
+  }
+  if (degree && (!dev_deg || !accumulate) && ntracked > 0)
+    CUDA_TRY(cudaMemsetAsync(d_deg, 0, ntracked * sizeof(uint32_t), c->stream));
+  if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
+  if (hi > lo) {
+    clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+    a.degree = d_deg;
+    a.track_shift = track_shift;
+    a.ring = reinterpret_cast<uint2*>(ring);
+    a.ring_mask = ring ? static_cast<unsigned long long>(ring_cap - 1) : 0ull;
+    if ((rc = launch_walk<clg::kWalkFold>(c, a))) return rc;
+  }
+  if (degree && !dev_deg && ntracked > 0)
+    CUDA_TRY(cudaMemcpyAsync(degree, d_deg, ntracked * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  if (count) *count = static_cast<int64_t>(c->sc_host->fold[0]);
+  if (checksum) *checksum = c->sc_host->fold[1];
+  c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);
+  if (n_flagged) *n_flagged = c->last_flagged;
+  return CLGEN_OK;
+}
+
+int clgen_dev_flagged_nodes(clgen_dev_ctx* c, int64_t* out, int64_t cap, int64_t* n) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  const int64_t k = c->last_flagged < kFlagCap ? c->last_flagged : kFlagCap;
+  const int64_t m = k < cap ? k : cap;
+  if (m > 0) {
+    CUDA_TRY(cudaMemcpyAsync(out, c->flagged, m * sizeof(int64_t), cudaMemcpyDefault, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  if (n) *n = c->last_flagged;
+  return CLGEN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Shared device helpers for the B200 Chung–Lu generator (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CLG_FULL 0xffffffffu
+
+namespace clg {
+
+// ---- splitmix64 finaliser (reference rng.hpp:11-16) ----------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// rng.hpp:20-22
+__host__ __device__ __forceinline__ uint64_t node_rng_key(uint64_t seed, int64_t u) {
+  return mix64(seed + static_cast<uint64_t>(u) * 0x9e3779b97f4a7c15ULL);
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+// Per-source xoshiro256++ stream, bit-identical to the reference RngStream
+// (rng.hpp:26-69).  Four words live in registers of the lane walking u.
+struct Xoshiro {
+  uint64_t s0, s1, s2, s3;
+
+  __device__ __forceinline__ void seed_key(uint64_t key) {
+    uint64_t sm = key;
+    uint64_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sm += 0x9e3779b97f4a7c15ULL;
+      uint64_t z = sm;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      w[i] = z ^ (z >> 31);
+    }
+    s0 = w[0]; s1 = w[1]; s2 = w[2]; s3 = w[3];
+    if ((s0 | s1 | s2 | s3) == 0) s0 = 1;  // rng.hpp:41
+  }
+
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t result = rotl64(s0 + s3, 23) + s0;
+    const uint64_t t = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= t;
+    s3 = rotl64(s3, 45);
+    return result;
+  }
+
+  // rng.hpp:58-63: (x>>11)*2^-53, exact zeros rejected (loop taken with
+  // probability 2^-53 per draw).
+  __device__ __forceinline__ double open01() {
+    for (;;) {
+      const double r = __dmul_rn(static_cast<double>(next() >> 11), 0x1.0p-53);
+      if (r > 0.0) return r;
+    }
+  }
+};
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-inclusive scan of an int64 value.
+__device__ __forceinline__ int64_t warp_inclusive_scan(int64_t x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(CLG_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int64_t warp_sum(int64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(CLG_FULL, x, o);
+  return x;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(CLG_FULL, x, o);
+  return x;
+}
+
+}  // namespace clg

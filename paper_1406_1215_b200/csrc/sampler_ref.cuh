@@ -1,0 +1,215 @@
+// Reference-stream Chung–Lu sampler: one lane walks one source chain with the
+// reference's own per-node xoshiro256++ stream, so every edge of an unflagged
+// node is bit-identical to clgen::edges_from_source
+// (/root/reference/proj/core/src/edge_skip.cpp:20-46).
+//
+// Work distribution: persistent warps; each warp refills idle lanes from a
+// warp-local batch of source ids taken from a global queue in index order
+// (heaviest sources first, since w is non-increasing — an LPT schedule).
+#pragma once
+
+#include "common.cuh"
+
+namespace clg {
+
+enum WalkMode : int { kWalkCount = 0, kWalkWrite = 1, kWalkFold = 2 };
+
+struct RefWalkArgs {
+  const double* __restrict__ w;  // non-increasing weights, n entries
+  int64_t n;
+  double S;
+  int64_t lo, hi;                // source slots [lo,hi)
+  const int64_t* sources;        // optional: slot i walks source sources[i] (create_edges)
+  uint64_t seed;
+  unsigned long long* queue;     // next unclaimed source (starts at lo)
+  // count mode
+  int32_t* counts;               // counts[slot-lo]
+  // write mode
+  const int64_t* offsets;        // offsets[slot-lo]: first output position of the slot
+  uint2* pairs;                  // (u,v) as uint32 pairs
+  int64_t cap;
+  // fold mode
+  uint32_t* degree;              // tracked undirected degrees, degree[x >> track_shift]
+  int track_shift;
+  uint2* ring;                   // optional emission ring (power-of-two capacity)
+  unsigned long long ring_mask;
+  unsigned long long* ring_head;
+  unsigned long long* fold_out;  // [0] edges, [1] checksum
+  // guard
+  unsigned long long* flag_count;
+  int64_t* flagged;              // first flag_cap flagged source ids
+  int64_t flag_cap;
+  unsigned long long* overflow;  // write mode: slots beyond cap
+};
+
+// Skip length exactly as edge_skip.cpp:9-16 computes it, with CUDA's libm.
+// `amb` is raised when the ratio lies within 2^-47 (relative) of an integer
+// >= 1: only there can glibc's log/log1p (<=1 ulp) and CUDA's (<=1 ulp)
+// disagree on the floor.  The survey measured 0 such ratios in 3.9e7
+// candidates.
+__device__ __forceinline__ int64_t skip_length_ref(double p, double r, bool& amb) {
+  const double ratio = __ddiv_rn(log(r), log1p(-p));
+  if (!(ratio < 9.0e18)) return INT64_MAX;
+  const double fl = floor(ratio);
+  const double dlo = ratio - fl;
+  const double dhi = (fl + 1.0) - ratio;
+  const double tol = ratio * 0x1p-47;
+  if ((dlo <= tol && fl >= 1.0) || dhi <= tol) amb = true;
+  return static_cast<int64_t>(ratio);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
+  constexpr int64_t kBatch = 256;
+  const int lane = lane_id();
+  const double* __restrict__ w = a.w;
+  const int64_t n = a.n;
+  const double S = a.S;
+
+  // warp-uniform batch state
+  int64_t b_next = 0, b_end = 0;
+  bool drained = false;
+  // per-warp ring reservation (fold mode)
+  unsigned long long r_next = 0, r_end = 0;
+
+  // lane state
+  int64_t u = -1, slot = 0, j = 0, out_pos = 0;
+  int32_t cnt = 0;
+  double p = 0.0, wu = 0.0;
+  bool amb = false;
+  Xoshiro rng;
+  uint64_t checksum = 0;
+  unsigned long long edges_total = 0;
+
+  for (;;) {
+    // ---------------------------------------------------------------- refill
+    const unsigned need = __ballot_sync(CLG_FULL, u < 0);
+    if (need && !drained) {
+      const int want = __popc(need);
+      const int r = __popc(need & lanemask_lt());
+      const bool me = (need >> lane) & 1u;
+      int64_t mine = -1;
+      const int64_t take1 = clg::imin64(b_end - b_next, want);
+      if (me && r < take1) mine = b_next + r;
+      b_next += take1;
+      if (want > take1) {
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(a.queue, (unsigned long long)kBatch);
+        g = __shfl_sync(CLG_FULL, g, 0);
+        if (static_cast<int64_t>(g) >= a.hi) {
+          drained = true;
+          b_next = b_end = a.hi;
+        } else {
+          b_next = static_cast<int64_t>(g);
+          b_end = clg::imin64(b_next + kBatch, a.hi);
+          const int64_t take2 = clg::imin64(b_end - b_next, want - take1);
+          if (me && r >= take1 && r - take1 < take2) mine = b_next + (r - take1);
+          b_next += take2;
+        }
+      }
+      if (mine >= 0) {
+        slot = mine - a.lo;
+        u = a.sources ? a.sources[mine] : mine;
+        j = u + 1;
+        cnt = 0;
+        amb = false;
+        wu = w[u];
+        if (MODE == kWalkWrite) out_pos = a.offsets[slot];
+        if (j < n && S > 0.0) {
+          rng.seed_key(node_rng_key(a.seed, u));
+          p = fmin(__ddiv_rn(__dmul_rn(wu, w[j]), S), 1.0);
+        } else {
+          p = 0.0;
+        }
+      }
+    }
+    const unsigned live = __ballot_sync(CLG_FULL, u >= 0);
+    if (!live) {
+      if (drained) break;
+      continue;
+    }
+
+    // ------------------------------------------------------------------ step
+    bool accepted = false;
+    int64_t v = 0;
+    bool finish = false;
+    if (u >= 0) {
+      if (!(j < n && p > 0.0)) {
+        finish = true;  // edge_skip.cpp:31 loop condition
+      } else {
+        int64_t delta = 0;
+        if (p < 1.0) delta = skip_length_ref(p, rng.open01(), amb);
+        if (delta >= n - j) {
+          finish = true;  // edge_skip.cpp:34
+        } else {
+          v = j + delta;
+          const double q = fmin(__ddiv_rn(__dmul_rn(wu, w[v]), S), 1.0);
+          const double r2 = rng.open01();
+          accepted = r2 < __ddiv_rn(q, p);  // edge_skip.cpp:38
+          p = q;
+          j = v + 1;
+        }
+      }
+    }
+
+    if (accepted) {
+      ++cnt;
+      if (MODE == kWalkWrite) {
+        if (out_pos < a.cap) {
+          a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
+        } else {
+          atomicAdd(a.overflow, 1ull);
+        }
+        ++out_pos;
+      } else if (MODE == kWalkFold) {
+        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(v));
+        ++edges_total;
+        if (a.degree && (v & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
+      }
+    }
+    if (MODE == kWalkFold && a.ring) {
+      const unsigned am = __ballot_sync(CLG_FULL, accepted);
+      if (am) {
+        const unsigned k = __popc(am);
+        const unsigned rk = __popc(am & lanemask_lt());
+        const unsigned long long rem = r_end - r_next;
+        unsigned long long nb = 0;
+        if (rem < k) {
+          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);
+          nb = __shfl_sync(CLG_FULL, nb, 0);
+        }
+        if (accepted) {
+          const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);
+          a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
+        }
+        if (rem < k) {
+          r_next = nb + (k - rem);
+          r_end = nb + 2048ull;
+        } else {
+          r_next += k;
+        }
+      }
+    }
+    if (u >= 0 && (finish || !(j < n && p > 0.0))) {
+      if (MODE == kWalkCount) a.counts[slot] = cnt;
+      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+      if (amb) {
+        const unsigned long long idx = atomicAdd(a.flag_count, 1ull);
+        if (static_cast<int64_t>(idx) < a.flag_cap) a.flagged[idx] = u;
+      }
+      u = -1;
+    }
+  }
+
+  if (MODE == kWalkFold) {
+    checksum = warp_sum_u64(checksum);
+    edges_total = warp_sum_u64(edges_total);
+    if (lane == 0) {
+      atomicAdd(&a.fold_out[0], edges_total);
+      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
+    }
+  }
+}
+
+}  // namespace clg

@@ -1,0 +1,131 @@
+"""Per-rank runtime around the device generator (the generate_on_rank analogue,
+/root/reference/proj/core/src/runtime.cpp:46-91): weight distribution to the
+ranks, the level-1 UCP plan over the GPUs, and end-to-end measurement helpers
+used by bench.py.  One process per GPU; torch.distributed (NCCL) carries the
+plan's tiny collectives.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+from . import api, workloads
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def shared_weights(config: str, n: int | None, world: int, rank: int, local: int) -> np.ndarray:
+    """Rank 0 synthesises the workload's weights; the other ranks receive them
+    over NCCL (every rank holds all of w)."""
+    if world == 1:
+        return workloads.make(config, n)
+    import torch
+    import torch.distributed as dist
+    meta = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+    w = None
+    if rank == 0:
+        w = workloads.make(config, n)
+        meta[0] = w.size
+    dist.broadcast(meta, 0)
+    t = (torch.from_numpy(w).to(f"cuda:{local}") if rank == 0
+         else torch.empty(int(meta[0]), dtype=torch.float64, device=f"cuda:{local}"))
+    dist.broadcast(t, 0)
+    out = t.cpu().numpy() if rank != 0 else w
+    del t
+    torch.cuda.empty_cache()
+    return out
+
+
+def plan(ws: api.WeightSequence, world: int, rank: int) -> np.ndarray:
+    """Level-1 UCP boundaries over `world` GPUs, bit-identical to
+    plan_ucp_oracle(ws, world) (partition.cpp:159-203)."""
+    if world == 1:
+        return np.array([0, ws.size()], np.int64)
+    from . import plan as _plan
+    return _plan.plan_ucp_distributed(ws, world, rank)
+
+
+def expected_edges(w: np.ndarray, S: float, lo: int, hi: int) -> float:
+    """Expected edges of sources [lo,hi) (unclamped, an upper bound of the
+    clamped mean) plus a 6-sigma margin: capacity sizing only."""
+    if hi <= lo or not S > 0:
+        return 0.0
+    suffix = S - np.cumsum(w, dtype=np.float64)
+    e = float((w[lo:hi] / S * suffix[lo:hi]).sum())
+    return e + 6.0 * np.sqrt(max(e, 1.0))
+
+
+def ncu_traffic(config: str, mode: str):
+    """DRAM bytes per sampler launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(f"{config}:{mode}")
+    except Exception:
+        return None
+
+
+def e2e_measure(args, w_host: np.ndarray, world: int, rank: int, local: int, lo: int, hi: int,
+                seed: int, materialise: bool) -> dict:
+    """The same metric through the public API with HOST buffers: every step
+    copies the weights host->device (pinned), recomputes S and the plan, runs
+    the generator and reads the result back (edges for materialised configs,
+    count/checksum/tracked degrees for streaming ones)."""
+    import torch
+    n = int(w_host.size)
+    pinned = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = w_host
+    dev = api.Device(local)
+    stream = dev.torch_stream()
+    ring = None
+    host_out = None
+    deg_host = None
+    if materialise:
+        cap = int(expected_edges(w_host, float(np.sum(w_host)), lo, hi) * 1.01 + 1_000_000)
+        host_out = torch.empty((cap, 2), dtype=torch.int32, pin_memory=True)
+    else:
+        ring = torch.empty((1 << args.ring_log2, 2), dtype=torch.int32, device=f"cuda:{local}")
+        ntr = (n + (1 << args.track_shift) - 1) >> args.track_shift
+        deg_host = torch.zeros(ntr, dtype=torch.int32, pin_memory=True)
+
+    def one():
+        dev.set_weights(pinned)                      # H2D (n * 8 bytes)
+        S = dev.blocked_sum()
+        ws = api.WeightSequence(w_host, S, None, dev)
+        b = plan(ws, world, rank)
+        a, z = int(b[rank]), int(b[rank + 1])
+        if materialise:
+            e = api.create_edges_range(ws, S, a, z, seed, out=host_out)  # D2H of the edges
+            return int(e.shape[0]), int(e.shape[0]) * 8
+        r = api.stream_range(ws, S, a, z, seed, mode=args.mode, track_shift=args.track_shift,
+                             degree=deg_host.numpy(), ring=ring)     # D2H of tracked degrees
+        return r.count, deg_host.numel() * 4 + 16
+
+    one()
+    torch.cuda.synchronize()
+    total_ms, edges = 0.0, 0
+    d2h = 0
+    for _ in range(args.steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        c, d2h = one()
+        ev1.record(stream)
+        ev1.synchronize()
+        total_ms += ev0.elapsed_time(ev1)
+        edges += c
+    ms = total_ms / args.steps
+    e_step = edges // args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e = torch.tensor([e_step], dtype=torch.int64, device="cuda")
+        dist.all_reduce(e)
+        ms, e_step = float(t[0]), int(e[0])
+    dev.close()
+    return {"value": e_step / (ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": n * 8,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms}

@@ -1,0 +1,151 @@
+"""GPU parity tests of the reference-stream sampler against the oracle and the
+golden vectors of the real reference (bit-exact: integer edge lists)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1406_1215_b200 import api as _api
+    return _api
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+def test_blocked_sum_bit_exact(api, port):
+    meta = json.load(open(os.path.join(GOLDEN, "meta.json")))
+    for name in meta:
+        g = load(f"edges_{name}.npz")
+        assert api.blocked_sum(g["w"]) == float(g["S"][0]), name
+    rng = np.random.default_rng(3)
+    for n in (1, 4095, 4096, 4097, 100_000, 1_234_567):
+        x = rng.uniform(0, 1e3, n) * rng.choice([1e-6, 1.0, 1e6], n)
+        assert api.blocked_sum(x) == port.blocked_sum(x), n
+    s = json.load(open(os.path.join(GOLDEN, "scalars.json")))
+    S = api.blocked_sum(np.full(10_000_000, 50.0))
+    assert np.array([S]).view(np.uint64)[0] == s["c2_S_bits"]
+
+
+def test_serial_cl_matches_golden(api):
+    meta = json.load(open(os.path.join(GOLDEN, "meta.json")))
+    for name, m in meta.items():
+        g = load(f"edges_{name}.npz")
+        ws = api.make_weight_sequence(g["w"])
+        assert ws.sum_S == float(g["S"][0])
+        for seed in m["seeds"]:
+            edges, flagged = api.serial_cl(ws, seed, return_flagged=True)
+            assert flagged == 0
+            np.testing.assert_array_equal(edges, g[f"edges_{seed}"], err_msg=f"{name}/{seed}")
+        if "range_lo_hi" in g:
+            lo, hi = (int(x) for x in g["range_lo_hi"])
+            np.testing.assert_array_equal(
+                api.create_edges_range(ws, ws.sum_S, lo, hi, m["seeds"][0]), g["edges_range"])
+            np.testing.assert_array_equal(
+                api.create_edges(ws, ws.sum_S, g["list_sources"], m["seeds"][0]), g["edges_list"])
+
+
+def test_contract_errors(api):
+    ws = api.make_weight_sequence([2.0, 2.0, 2.0, 2.0])
+    with pytest.raises(api.error, match="bad node range"):
+        api.create_edges_range(ws, ws.sum_S, 0, 5, 1)
+    with pytest.raises(api.error, match="bad node range"):
+        api.create_edges_range(ws, ws.sum_S, 3, 2, 1)
+    with pytest.raises(api.error, match="out of range"):
+        api.create_edges(ws, ws.sum_S, [99], 1)
+    with pytest.raises(api.error, match="unsorted at position 2"):
+        api.make_weight_sequence([3.0, 2.0, 2.5])
+    # last node has no destinations (test_edge_skip.cpp:86-90)
+    assert len(api.create_edges(ws, ws.sum_S, [3], 1)) == 0
+    one = api.make_weight_sequence([5.0])
+    assert len(api.serial_cl(one, 3)) == 0
+    empty = api.make_weight_sequence(np.zeros(0))
+    assert len(api.serial_cl(empty, 3)) == 0
+
+
+def test_random_instances_vs_oracle(api, port):
+    rng = np.random.default_rng(11)
+    for t in range(20):
+        n = int(rng.integers(2, 3000))
+        w = np.sort(rng.uniform(0.0, rng.choice([1.0, 10.0, 100.0]), n))[::-1].copy()
+        if t % 5 == 0:
+            w[: max(1, n // 50)] *= 50.0  # saturated head: p clamps at 1
+            w = np.sort(w)[::-1].copy()
+        if t % 7 == 0:
+            w[-n // 3:] = 0.0  # zero-weight tail
+        ws = api.make_weight_sequence(w)
+        seed = int(rng.integers(0, 2**64, dtype=np.uint64))
+        got, flagged = api.serial_cl(ws, seed, return_flagged=True)
+        exp, cnt, _, _ = port.create_edges_range(w, ws.sum_S, 0, n, seed)
+        assert flagged == 0
+        np.testing.assert_array_equal(got, exp, err_msg=f"trial {t}")
+        counts = api.edge_counts(ws, ws.sum_S, 0, n, seed)
+        np.testing.assert_array_equal(counts, port.edge_counts(w, ws.sum_S, 0, n, seed))
+
+
+def test_c1_continuous_materialised_and_streamed(api, port):
+    s = json.load(open(os.path.join(GOLDEN, "scalars.json")))["c1_continuous"]
+    w = port.synth_powerlaw(1_000_000, 2.5, 10.0, 1000.0, 1)
+    ws = api.make_weight_sequence(w)
+    assert np.array([ws.sum_S]).view(np.uint64)[0] == s["S_bits"]
+    edges, flagged = api.serial_cl(ws, 7, return_flagged=True)
+    assert flagged == 0
+    assert len(edges) == s["edges"]
+    exp, _, cks, deg = port.create_edges_range(w, ws.sum_S, 0, w.size, 7, degree=True)
+    np.testing.assert_array_equal(edges, exp)
+    res = api.stream_range(ws, ws.sum_S, 0, w.size, 7, track_shift=0)
+    assert res.count == s["edges"]
+    assert res.checksum == s["checksum"] == cks
+    np.testing.assert_array_equal(res.degree.astype(np.int64), deg)
+    res4 = api.stream_range(ws, ws.sum_S, 0, w.size, 7, track_shift=4)
+    np.testing.assert_array_equal(res4.degree.astype(np.int64), deg[::16])
+
+
+def test_device_output_buffer(api, port):
+    import torch
+    w = port.synth_powerlaw(50_000, 2.5, 2.0, 200.0, 3)
+    ws = api.make_weight_sequence(w)
+    exp, cnt, _, _ = port.create_edges_range(w, ws.sum_S, 100, 40_000, 9)
+    out = torch.empty((cnt + 10, 2), dtype=torch.int32, device="cuda")
+    got = api.create_edges_range(ws, ws.sum_S, 100, 40_000, 9, out=out)
+    np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), exp)
+    small = torch.empty((cnt // 2, 2), dtype=torch.int32, device="cuda")
+    with pytest.raises(api.error, match="exceed capacity"):
+        api.create_edges_range(ws, ws.sum_S, 100, 40_000, 9, out=small)
+
+
+def test_ring_emission_matches_checksum(api, port):
+    import torch
+    w = port.synth_powerlaw(200_000, 2.5, 5.0, 500.0, 4)
+    ws = api.make_weight_sequence(w)
+    _, cnt, cks, _ = port.create_edges_range(w, ws.sum_S, 0, w.size, 5, materialise=False)
+    cap = 1 << 22
+    assert cnt < cap // 2
+    ring = torch.zeros((cap, 2), dtype=torch.int32, device="cuda")
+    res = api.stream_range(ws, ws.sum_S, 0, w.size, 5, ring=ring)
+    assert res.count == cnt and res.checksum == cks
+    # every edge landed in the ring exactly once (reservation tails stay zero)
+    r = ring.cpu().numpy().view(np.uint32).astype(np.uint64)
+    nz = r[(r[:, 0] != 0) | (r[:, 1] != 0)]
+    assert len(nz) == cnt
+    assert int(mix64_np((nz[:, 0] << np.uint64(32)) | nz[:, 1]).sum(dtype=np.uint64)) == cks
+
+
+def mix64_np(z):
+    """Vectorised splitmix64 finaliser (rng.hpp:11-16), wrapping uint64."""
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
