@@ -60,7 +60,7 @@ __device__ __forceinline__ int64_t skip_length_ref(double p, double r, bool& amb
 
 template <int MODE>
 __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
-  constexpr int64_t kBatch = 256;
+  constexpr int64_t kBatch = 32;
   const int lane = lane_id();
   const double* __restrict__ w = a.w;
   const int64_t n = a.n;
