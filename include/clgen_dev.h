@@ -117,6 +117,34 @@ int clgen_dev_stream_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi,
                            uint32_t* ring, int64_t ring_cap, int64_t* count, uint64_t* checksum,
                            int64_t* n_flagged);
 
+/*
+ * Level-1 uniform-cost partition (UCP) of this context's weights into P
+ * consecutive blocks, bit-identical to plan_ucp_oracle(ws, P)
+ * (partition.cpp:159-203) and hence to the SPMD plan_ucp (:107-157).  The
+ * reference's P-blocked sequential FP64 folds (block weights, sigma_u, C_u)
+ * are replayed exactly by a parallel per-binade integer scan.
+ * boundaries: P+1 int64 (host or device).  cum_costs (optional, host or
+ * device, n doubles) receives the finalized C_u (cost.cpp:48-51).
+ * P < 1 returns CLGEN_EINVAL ("plan_ucp_oracle: P must be >= 1").
+ */
+int clgen_dev_plan_ucp(clgen_dev_ctx* ctx, int P, int64_t* boundaries, double* cum_costs);
+
+/*
+ * The same plan split into per-rank device phases for G GPUs (rank g calls
+ * them on its own context; the caller performs the collectives between them,
+ * folding gathered values in rank order as comm.cpp:39-53 does):
+ *   1. block weight of rank block g, a fold from 0.0 (partition.cpp:115-116)
+ *   2. block_cumulative from sigma_start (cost.cpp:24-46); returns z_g
+ *   3. boundaries found in block g given Z_g and Z_bar: found[0..G] (host or
+ *      device int64) receives u for every k crossed inside the block, n
+ *      elsewhere; the element-wise MIN over ranks is the plan.
+ */
+int clgen_dev_plan_block_weight(clgen_dev_ctx* ctx, int G, int g, double* block_weight);
+int clgen_dev_plan_block_costs(clgen_dev_ctx* ctx, int G, int g, double sigma_start, double S,
+                               double* block_cost);
+int clgen_dev_plan_block_boundaries(clgen_dev_ctx* ctx, int G, int g, double z_offset,
+                                    double z_bar, int64_t* found);
+
 /* Ids of the sources flagged by the last generation call (up to cap). */
 int clgen_dev_flagged_nodes(clgen_dev_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
 

@@ -67,6 +67,11 @@ def _declare(L):
     L.clgen_dev_stream_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, C.c_int, _vp,
                                          C.c_int, _vp, _i64, _i64p, _u64p, _i64p]
     L.clgen_dev_flagged_nodes.argtypes = [_vp, _i64p, _i64, _i64p]
+    L.clgen_dev_plan_ucp.argtypes = [_vp, C.c_int, _vp, _vp]
+    L.clgen_dev_plan_block_weight.argtypes = [_vp, C.c_int, C.c_int, _dp]
+    L.clgen_dev_plan_block_costs.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+    L.clgen_dev_plan_block_boundaries.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double,
+                                                  _vp]
     return L
 
 
@@ -77,7 +82,8 @@ EXPORTS = (
     "clgen_dev_last_kernel_ms", "clgen_dev_set_weights", "clgen_dev_num_nodes",
     "clgen_dev_weights", "clgen_dev_blocked_sum", "clgen_dev_blocked_sum_array", "clgen_dev_create_edges_range",
     "clgen_dev_create_edges", "clgen_dev_edge_counts", "clgen_dev_stream_range",
-    "clgen_dev_flagged_nodes",
+    "clgen_dev_flagged_nodes", "clgen_dev_plan_ucp", "clgen_dev_plan_block_weight",
+    "clgen_dev_plan_block_costs", "clgen_dev_plan_block_boundaries",
 )
 
 

@@ -315,3 +315,18 @@ def stream_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
                                    int(accumulate), _addr(ring) if ring is not None else None,
                                    ring_cap, C.byref(cnt), C.byref(cks), C.byref(nfl)))
     return StreamResult(cnt.value, cks.value, nfl.value, degree)
+
+
+def plan_ucp(ws: WeightSequence, P: int, with_costs: bool = False):
+    """Level-1 UCP on the device, bit-identical to plan_ucp_oracle(ws, P)
+    (partition.cpp:159-203).  Returns int64[P+1] boundaries, plus the
+    finalized C_u (float64[n]) when ``with_costs``."""
+    if P < 1:
+        raise error("plan_ucp_oracle: P must be >= 1")
+    b = np.empty(P + 1, np.int64)
+    cum = np.empty(max(ws.size(), 1), np.float64) if with_costs else None
+    check(_lib.lib().clgen_dev_plan_ucp(ws.device.handle, int(P), b.ctypes.data,
+                                        cum.ctypes.data if with_costs else None))
+    if with_costs:
+        return b, cum[: ws.size()]
+    return b

@@ -9,11 +9,15 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "../../include/clgen_dev.h"
 #include "common.cuh"
+#include "exact_fold.cuh"
+#include "plan.cuh"
 #include "sampler_ref.cuh"
 #include "scan.cuh"
 #include "weights.cuh"
@@ -86,6 +90,7 @@ struct Scalars {
   unsigned long long first_negative;
   int64_t total;
   double S;
+  double fold_final;
 };
 
 constexpr int64_t kFlagCap = 4096;
@@ -103,7 +108,8 @@ struct clgen_dev_ctx {
   Scalars* sc_host = nullptr;  // pinned mirror
   int64_t* flagged = nullptr;  // device, kFlagCap
   int64_t last_flagged = 0;
-  DevBuf counts, offsets, tiles, pairs, partials, degree, sources;
+  DevBuf counts, offsets, tiles, pairs, partials, degree, sources, foldtmp, cum, found;
+  int plan_G = 0;  // blocks of the cost profile currently held in `cum`
   int walk_blocks[3] = {0, 0, 0};
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
@@ -221,6 +227,121 @@ int blocked_sum_impl(clgen_dev_ctx* c, const double* d, int64_t n, double* S) {
   return CLGEN_OK;
 }
 
+// ---- exact sequential-fold replay (exact_fold.cuh) -------------------------
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Folds x[0..m) left to right from s0 exactly as a sequential FP64 loop
+// would; *final_host receives s_m.  out_mode/out/w/S per clg::FoldOut.
+int run_fold(clgen_dev_ctx* c, const double* x, int64_t m, double s0, int out_mode, double* out,
+             const double* w, double S, double* final_host) {
+  if (m == 0) {
+    *final_host = s0;
+    return CLGEN_OK;
+  }
+  const int64_t T = (m + clg::kFoldTile - 1) / clg::kFoldTile;
+  const size_t b_tsum = align_up(T * sizeof(double)), b_app = align_up((T + 1) * sizeof(double)),
+               b_fun = align_up(T * sizeof(clg::Fn)), b_bin = align_up(T * sizeof(int)),
+               b_start = align_up(T * sizeof(double)), b_slow = align_up(T);
+  CUDA_TRY(c->foldtmp.ensure(b_tsum + b_app + b_fun + b_bin + b_start + b_slow));
+  char* base = c->foldtmp.as<char>();
+  clg::FoldArgs a;
+  a.x = x;
+  a.m = m;
+  a.s0 = s0;
+  a.tsum = reinterpret_cast<double*>(base);
+  a.approx = reinterpret_cast<double*>(base + b_tsum);
+  a.tfun = reinterpret_cast<clg::Fn*>(base + b_tsum + b_app);
+  a.tbin = reinterpret_cast<int*>(base + b_tsum + b_app + b_fun);
+  a.start = reinterpret_cast<double*>(base + b_tsum + b_app + b_fun + b_bin);
+  a.slow = reinterpret_cast<unsigned char*>(base + b_tsum + b_app + b_fun + b_bin + b_start);
+  a.final_out = &c->sc->fold_final;
+  a.out_mode = out_mode;
+  a.out = out;
+  a.w = w;
+  a.S = S;
+  const unsigned g = static_cast<unsigned>(T);
+  clg::fold_tile_sums_kernel<<<g, clg::kFoldThreads, 0, c->stream>>>(a);
+  clg::fold_approx_prefix_kernel<<<1, 1024, 0, c->stream>>>(a, T);
+  clg::fold_tile_fun_kernel<<<g, clg::kFoldThreads, 0, c->stream>>>(a);
+  clg::fold_spine_kernel<<<1, 32, 0, c->stream>>>(a, T);
+  c->launches += 4;
+  if (out_mode != clg::kFoldNone) {
+    clg::fold_emit_kernel<<<g, clg::kFoldThreads, 0, c->stream>>>(a);
+    ++c->launches;
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(&c->sc_host->fold_final, &c->sc->fold_final, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *final_host = c->sc_host->fold_final;
+  return CLGEN_OK;
+}
+
+// cost.cpp:15-22
+void block_bounds_host(int64_t n, int P, int rank, int64_t* lo, int64_t* hi) {
+  const int64_t q = n / P, r = n % P;
+  *lo = static_cast<int64_t>(rank) * q + (rank < r ? rank : r);
+  *hi = *lo + q + (rank < r ? 1 : 0);
+}
+
+int plan_args_ok(clgen_dev_ctx* c, int G, int g) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (G < 1 || g < 0 || g >= G) return fail(CLGEN_EINVAL, "block_bounds: bad rank/P");
+  return set_device(c);
+}
+
+int ensure_cum(clgen_dev_ctx* c, int G) {
+  CUDA_TRY(c->cum.ensure((c->n > 0 ? c->n : 1) * sizeof(double)));
+  c->plan_G = G;
+  return CLGEN_OK;
+}
+
+int block_weight_impl(clgen_dev_ctx* c, int G, int g, double* bw) {
+  int64_t lo, hi;
+  block_bounds_host(c->n, G, g, &lo, &hi);
+  return run_fold(c, c->w + lo, hi - lo, 0.0, clg::kFoldNone, nullptr, nullptr, 0.0, bw);
+}
+
+// block_cumulative (cost.cpp:24-46): c_u from the exact sigma fold, then the
+// exact cumulative fold (first element cum = c, i.e. a fold from 0.0).
+int block_costs_impl(clgen_dev_ctx* c, int G, int g, double sigma_start, double S, double* z) {
+  int64_t lo, hi;
+  block_bounds_host(c->n, G, g, &lo, &hi);
+  int rc = ensure_cum(c, G);
+  if (rc) return rc;
+  double* cum = c->cum.as<double>();
+  if (hi == lo) {
+    *z = 0.0;
+    return CLGEN_OK;
+  }
+  if (S > 0.0) {
+    double sigma_end;
+    if ((rc = run_fold(c, c->w + lo, hi - lo, sigma_start, clg::kFoldNodeCost, cum + lo, c->w + lo, S,
+                       &sigma_end)))
+      return rc;
+  } else {  // S == 0 degenerates to unit costs (cost.cpp:34-36)
+    clg::fill_f64_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(cum, lo, hi, 1.0);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return run_fold(c, cum + lo, hi - lo, 0.0, clg::kFoldInclusive, cum + lo, nullptr, 0.0, z);
+}
+
+int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, double z_bar, long long* d_found) {
+  int64_t lo, hi;
+  block_bounds_host(c->n, G, g, &lo, &hi);
+  if (!(z_bar > 0.0)) return fail(CLGEN_EINVAL, "partition_of: Z_bar must be > 0");
+  if (hi > lo) {
+    const int64_t m = hi - lo;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, c->num_sms * 16));
+    clg::ucp_transitions_kernel<<<grid, 256, 0, c->stream>>>(c->cum.as<double>(), lo, hi, z_offset, z_bar, G,
+                                                           d_found);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return CLGEN_OK;
+}
+
 // Two-pass materialisation in the reference's emission order: count pass,
 // decoupled-lookback scan of the per-slot counts, replay pass writing each
 // slot's edges at its scanned offset.
@@ -325,6 +446,9 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->partials.release();
   c->degree.release();
   c->sources.release();
+  c->foldtmp.release();
+  c->cum.release();
+  c->found.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -505,6 +629,98 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   if (checksum) *checksum = c->sc_host->fold[1];
   c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);
   if (n_flagged) *n_flagged = c->last_flagged;
+  return CLGEN_OK;
+}
+
+int clgen_dev_plan_block_weight(clgen_dev_ctx* c, int G, int g, double* block_weight) {
+  int rc = plan_args_ok(c, G, g);
+  if (rc) return rc;
+  if (!block_weight) return fail(CLGEN_EINVAL, "plan_block_weight: null output");
+  return block_weight_impl(c, G, g, block_weight);
+}
+
+int clgen_dev_plan_block_costs(clgen_dev_ctx* c, int G, int g, double sigma_start, double S,
+                               double* block_cost) {
+  int rc = plan_args_ok(c, G, g);
+  if (rc) return rc;
+  if (!block_cost) return fail(CLGEN_EINVAL, "plan_block_costs: null output");
+  return block_costs_impl(c, G, g, sigma_start, S, block_cost);
+}
+
+int clgen_dev_plan_block_boundaries(clgen_dev_ctx* c, int G, int g, double z_offset, double z_bar,
+                                    int64_t* found) {
+  int rc = plan_args_ok(c, G, g);
+  if (rc) return rc;
+  if (!found) return fail(CLGEN_EINVAL, "plan_block_boundaries: null output");
+  if (c->plan_G != G) return fail(CLGEN_EINVAL, "plan_block_boundaries: costs of block %d/%d not computed", g, G);
+  CUDA_TRY(c->found.ensure((G + 1) * sizeof(long long)));
+  long long* d = c->found.as<long long>();
+  clg::fill_i64_kernel<<<1, 256, 0, c->stream>>>(d, G + 1, static_cast<long long>(c->n));
+  ++c->launches;
+  if ((rc = block_boundaries_impl(c, G, g, z_offset, z_bar, d))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(found, d, (G + 1) * sizeof(long long), cudaMemcpyDefault, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
+int clgen_dev_plan_ucp(clgen_dev_ctx* c, int P, int64_t* boundaries, double* cum_costs) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (P < 1) return fail(CLGEN_EINVAL, "plan_ucp_oracle: P must be >= 1");
+  if (!boundaries) return fail(CLGEN_EINVAL, "plan_ucp: null boundaries");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  std::vector<long long> b(static_cast<size_t>(P) + 1, 0);
+  if (n == 0) {  // trivial_plan (partition.cpp:89-96)
+    CUDA_TRY(cudaMemcpy(boundaries, b.data(), b.size() * sizeof(long long), cudaMemcpyDefault));
+    return CLGEN_OK;
+  }
+  double Scan;  // the canonical sum_S (weights.cpp:54)
+  if ((rc = blocked_sum_impl(c, c->w, n, &Scan))) return rc;
+  // partition.cpp:165-170: block weights, each a fold from 0.0
+  std::vector<double> bw(P), bc(P);
+  for (int i = 0; i < P; ++i)
+    if ((rc = block_weight_impl(c, P, i, &bw[i]))) return rc;
+  // :172-177: block_cumulative from the rank-ordered prefix of block weights
+  for (int i = 0; i < P; ++i) {
+    double sp = 0.0;
+    for (int j = 0; j < i; ++j) sp += bw[j];
+    if ((rc = block_costs_impl(c, P, i, sp, Scan, &bc[i]))) return rc;
+  }
+  double total = 0.0;  // :180-181
+  for (int j = 0; j < P; ++j) total += bc[j];
+  const double z_bar = total / P;
+  CUDA_TRY(c->found.ensure((P + 1) * sizeof(long long)));
+  long long* d = c->found.as<long long>();
+  clg::fill_i64_kernel<<<1, 256, 0, c->stream>>>(d, P + 1, static_cast<long long>(n));
+  ++c->launches;
+  for (int i = 0; i < P; ++i) {
+    double zp = 0.0;
+    for (int j = 0; j < i; ++j) zp += bc[j];
+    if ((rc = block_boundaries_impl(c, P, i, zp, z_bar, d))) return rc;
+    if (cum_costs) {
+      int64_t lo, hi;
+      block_bounds_host(n, P, i, &lo, &hi);
+      if (hi > lo) {
+        if (is_device_ptr(cum_costs)) {
+          clg::add_offset_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(c->cum.as<double>(), cum_costs, lo, hi, zp);
+        } else {
+          clg::add_offset_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(c->cum.as<double>(), c->cum.as<double>(), lo,
+                                                                      hi, zp);
+        }
+        ++c->launches;
+        CUDA_TRY(cudaGetLastError());
+      }
+    }
+  }
+  if (cum_costs && !is_device_ptr(cum_costs))
+    CUDA_TRY(cudaMemcpyAsync(cum_costs, c->cum.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(b.data(), d, (P + 1) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  b[0] = 0;
+  b[P] = n;
+  if (cum_costs && !is_device_ptr(cum_costs)) c->plan_G = 0;  // cum now holds finalized values
+  CUDA_TRY(cudaMemcpy(boundaries, b.data(), b.size() * sizeof(long long), cudaMemcpyDefault));
   return CLGEN_OK;
 }
 
