@@ -96,6 +96,23 @@ int clgen_dev_create_edges(clgen_dev_ctx* ctx, double S, const int64_t* sources,
                            uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count,
                            int64_t* n_flagged);
 
+/*
+ * Materialised generation with a selectable stream: CLGEN_STREAM_REFERENCE is
+ * exactly clgen_dev_create_edges_range; CLGEN_STREAM_COUNTER draws from the
+ * counter-based stream (statistically exact, deterministic per seed,
+ * independent of GPU count).  Output order: u ascending, then v ascending.
+ */
+int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,
+                             int stream_mode, uint32_t* pairs, int64_t cap, int64_t* count,
+                             int64_t* n_flagged);
+
+/* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
+ * w_last inside a class; default 1/8) and the hub split size in expected
+ * candidates (default 4096).  Changing them changes the generated graph. */
+int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);
+/* Size of the last counter plan: weight classes, split sources, work units. */
+int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* hubs, int64_t* units);
+
 /* Count pass only: per-source edge counts (int32, hi-lo entries, host or device). */
 int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,
                           int32_t* counts, int64_t* total, int64_t* n_flagged);

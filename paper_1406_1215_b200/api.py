@@ -136,6 +136,15 @@ class Device:
         check(_lib.lib().clgen_dev_blocked_sum(self._h, C.byref(out)))
         return out.value
 
+    def set_counter_params(self, class_eps: float = 0.125, split_cap: float = 4096.0) -> None:
+        """Counter-stream weight-class width and hub split size (changes the graph)."""
+        check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, split_cap))
+
+    def counter_plan_info(self) -> dict:
+        k, h, u = C.c_int(), C.c_int64(), C.c_int64()
+        check(_lib.lib().clgen_dev_counter_plan_info(self._h, C.byref(k), C.byref(h), C.byref(u)))
+        return {"classes": k.value, "hubs": h.value, "units": u.value}
+
     def flagged_nodes(self) -> np.ndarray:
         n = C.c_int64()
         buf = np.empty(4096, np.int64)
@@ -330,3 +339,26 @@ def plan_ucp(ws: WeightSequence, P: int, with_costs: bool = False):
     if with_costs:
         return b, cum[: ws.size()]
     return b
+
+
+def generate_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
+                   mode: str = "counter", out=None):
+    """Materialised generation with either stream (uint32[m,2], u then v ascending)."""
+    L = _lib.lib()
+    sm = {"reference": STREAM_REFERENCE, "counter": STREAM_COUNTER}[mode]
+    cnt, nfl = C.c_int64(), C.c_int64()
+    if out is None:
+        rc = L.clgen_dev_generate_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF, sm,
+                                        None, 0, C.byref(cnt), C.byref(nfl))
+        if rc not in (_lib.CLGEN_OK, _lib.CLGEN_ERANGE):
+            check(rc)
+        total = cnt.value
+        buf = np.empty((max(total, 1), 2), np.uint32)
+        if total:
+            check(L.clgen_dev_generate_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF,
+                                             sm, buf.ctypes.data, total, C.byref(cnt),
+                                             C.byref(nfl)))
+        return buf[: cnt.value]
+    check(L.clgen_dev_generate_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF, sm,
+                                     _addr(out), int(out.shape[0]), C.byref(cnt), C.byref(nfl)))
+    return out[: cnt.value]

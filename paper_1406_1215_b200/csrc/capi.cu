@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "exact_fold.cuh"
 #include "plan.cuh"
+#include "sampler_ctr.cuh"
 #include "sampler_ref.cuh"
 #include "scan.cuh"
 #include "weights.cuh"
@@ -110,6 +111,15 @@ struct clgen_dev_ctx {
   int64_t last_flagged = 0;
   DevBuf counts, offsets, tiles, pairs, partials, degree, sources, foldtmp, cum, found;
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
+  // counter stream: weight-class segment table (per weights) and the hub
+  // split plan of the last source range
+  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, hub_units, split_pos, unit_counts;
+  int seg_K = 0;
+  bool seg_valid = false;
+  double seg_eps = 0.125;
+  double split_cap = 4096.0;
+  int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0;
+  int ctr_blocks[3] = {0, 0, 0};
   int walk_blocks[3] = {0, 0, 0};
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
@@ -342,6 +352,178 @@ int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, doubl
   return CLGEN_OK;
 }
 
+// ---- counter stream (sampler_ctr.cuh) ----------------------------------------
+int ensure_segments(clgen_dev_ctx* c) {
+  if (c->seg_valid) return CLGEN_OK;
+  const int kmax = 4096;
+  CUDA_TRY(c->seg_start.ensure((kmax + 1) * sizeof(int64_t)));
+  CUDA_TRY(c->seg_wfirst.ensure((kmax + 1) * sizeof(double)));
+  CUDA_TRY(c->seg_sure.ensure((kmax + 1) * sizeof(double)));
+  CUDA_TRY(c->seg_mass.ensure((kmax + 1) * sizeof(double)));
+  double eps = c->seg_eps;
+  for (int attempt = 0; attempt < 12; ++attempt, eps *= 2.0) {
+    clg::build_segments_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, eps, kmax, c->seg_start.as<int64_t>(),
+                                                        c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
+                                                        reinterpret_cast<int*>(&c->sc->total));
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    int K = 0;
+    CUDA_TRY(cudaMemcpyAsync(&K, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (K > 0) {
+      c->seg_K = K;
+      clg::Segments sg{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(), K};
+      clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
+      ++c->launches;
+      CUDA_TRY(cudaGetLastError());
+      c->seg_valid = true;
+      return CLGEN_OK;
+    }
+  }
+  return fail(CLGEN_EINVAL, "counter stream: weight range too wide for the class table");
+}
+
+clg::Segments segments(clgen_dev_ctx* c) {
+  return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(), c->seg_K};
+}
+
+// Hub split plan for sources [lo,hi): sources whose envelope-expected
+// candidate count exceeds split_cap are split into v-ranges of ~split_cap.
+int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
+  int rc = ensure_segments(c);
+  if (rc) return rc;
+  if (c->ctr_lo == lo && c->ctr_hi == hi) return CLGEN_OK;
+  // E_u <= w_u (1+eps): only sources with w_u >= cap/(1+eps) can be hubs
+  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, lo, hi, c->split_cap / (1.0 + 2.0 * c->seg_eps),
+                                                   reinterpret_cast<long long*>(&c->sc->total));
+  ++c->launches;
+  CUDA_TRY(cudaGetLastError());
+  long long fb = 0;
+  CUDA_TRY(cudaMemcpyAsync(&fb, &c->sc->total, sizeof fb, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int64_t H = fb - lo;
+  c->ctr_H = H;
+  int64_t hub_total = 0;
+  if (H > 0) {
+    CUDA_TRY(c->hub_units.ensure((H + 1) * sizeof(int64_t)));
+    CUDA_TRY(c->counts.ensure(H * sizeof(int64_t)));  // scratch: per-hub split counts
+    int64_t* splits = reinterpret_cast<int64_t*>(c->counts.p);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((H + 255) / 256, c->num_sms * 8));
+    clg::hub_splits_kernel<<<grid, 256, 0, c->stream>>>(c->w, c->n, S, lo, H, segments(c), c->seg_mass.as<double>(),
+                                                      c->split_cap, splits);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    // exclusive scan of split counts -> hub_units[0..H), total -> hub_units[H]
+    const int64_t ntiles = (H + clg::kScanTile - 1) / clg::kScanTile;
+    CUDA_TRY(c->tiles.ensure(ntiles * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(c->tiles.p, 0, ntiles * sizeof(unsigned long long), c->stream));
+    CUDA_TRY(cudaMemsetAsync(&c->sc->ticket, 0, sizeof(unsigned long long), c->stream));
+    clg::scan_lookback_kernel<int64_t><<<static_cast<unsigned>(ntiles), clg::kScanThreads, 0, c->stream>>>(
+        splits, c->hub_units.as<int64_t>(), H, c->tiles.as<unsigned long long>(), &c->sc->ticket,
+        c->hub_units.as<int64_t>() + H, 0);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(&hub_total, c->hub_units.as<int64_t>() + H, sizeof hub_total, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c->split_pos.ensure((hub_total + 1) * sizeof(int64_t)));
+    clg::hub_positions_kernel<<<grid, 256, 0, c->stream>>>(c->w, c->n, S, lo, H, segments(c), c->seg_mass.as<double>(),
+                                                         c->hub_units.as<int64_t>(), c->split_pos.as<int64_t>());
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    CUDA_TRY(c->hub_units.ensure(sizeof(int64_t)));
+    CUDA_TRY(c->split_pos.ensure(sizeof(int64_t)));
+  }
+  c->ctr_units = hub_total + (hi - lo - (H > 0 ? H : 0));
+  c->ctr_lo = lo;
+  c->ctr_hi = hi;
+  return CLGEN_OK;
+}
+
+clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed) {
+  clg::CtrWalkArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.w = c->w;
+  a.n = c->n;
+  a.S = S;
+  a.lo = lo;
+  a.hi = hi;
+  const uint64_t key = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
+  a.key0 = static_cast<uint32_t>(key);
+  a.key1 = static_cast<uint32_t>(key >> 32);
+  a.seg = segments(c);
+  a.H = c->ctr_H;
+  a.hub_units = c->hub_units.as<int64_t>();
+  a.total_units = c->ctr_units;
+  a.queue = &c->sc->queue;
+  a.overflow = &c->sc->overflow;
+  a.fold_out = c->sc->fold;
+  a.ring_head = &c->sc->ring_head;
+  return a;
+}
+
+template <int MODE>
+int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a) {
+  if (!c->ctr_blocks[MODE]) {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE>, 256, 0));
+    c->ctr_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+  clg::ctr_walk_kernel<MODE><<<c->ctr_blocks[MODE], 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>());
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  c->timed = true;
+  ++c->launches;
+  return CLGEN_OK;
+}
+
+// Materialised counter-stream generation (count pass, scan over units, write).
+int materialise_ctr(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed, uint32_t* pairs,
+                    int64_t cap, int64_t* count) {
+  if (cap < 0 || (cap > 0 && !pairs)) return fail(CLGEN_EINVAL, "generate_range: bad output buffer");
+  int rc = set_device(c);
+  if (rc) return rc;
+  if ((rc = reset_scalars(c, 0))) return rc;
+  if (hi == lo || !(S > 0.0)) {
+    if (count) *count = 0;
+    return CLGEN_OK;
+  }
+  if ((rc = ensure_ctr_plan(c, S, lo, hi))) return rc;
+  const int64_t U = c->ctr_units;
+  CUDA_TRY(c->unit_counts.ensure((U > 0 ? U : 1) * sizeof(int32_t)));
+  CUDA_TRY(c->offsets.ensure((U > 0 ? U : 1) * sizeof(int64_t)));
+  clg::CtrWalkArgs a = ctr_args(c, S, lo, hi, seed);
+  a.counts = c->unit_counts.as<int32_t>();
+  if ((rc = launch_ctr<clg::kWalkCount>(c, a))) return rc;
+  if ((rc = launch_scan(c, a.counts, c->offsets.as<int64_t>(), U))) return rc;
+  const bool dev_out = is_device_ptr(pairs);
+  uint2* d_pairs = reinterpret_cast<uint2*>(pairs);
+  if (!dev_out) {
+    if ((rc = fetch_scalars(c))) return rc;
+    const int64_t total = c->sc_host->total;
+    const int64_t stage = total < cap ? total : cap;
+    CUDA_TRY(c->pairs.ensure((stage > 0 ? stage : 1) * sizeof(uint2)));
+    d_pairs = c->pairs.as<uint2>();
+    cap = stage;
+  }
+  CUDA_TRY(cudaMemsetAsync(&c->sc->queue, 0, sizeof(unsigned long long), c->stream));
+  a.counts = nullptr;
+  a.offsets = c->offsets.as<int64_t>();
+  a.pairs = d_pairs;
+  a.cap = cap;
+  if ((rc = launch_ctr<clg::kWalkWrite>(c, a))) return rc;
+  if (!dev_out && cap > 0)
+    CUDA_TRY(cudaMemcpyAsync(pairs, d_pairs, cap * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  const int64_t total = c->sc_host->total;
+  if (count) *count = total;
+  if (total > cap)
+    return fail(CLGEN_ERANGE, "generate_range: %lld edges exceed capacity %lld", (long long)total, (long long)cap);
+  return CLGEN_OK;
+}
+
 // Two-pass materialisation in the reference's emission order: count pass,
 // decoupled-lookback scan of the per-slot counts, replay pass writing each
 // slot's edges at its scanned offset.
@@ -449,6 +631,13 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->foldtmp.release();
   c->cum.release();
   c->found.release();
+  c->seg_start.release();
+  c->seg_wfirst.release();
+  c->seg_sure.release();
+  c->seg_mass.release();
+  c->hub_units.release();
+  c->split_pos.release();
+  c->unit_counts.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -490,6 +679,9 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
     c->w_bytes = bytes;
   }
   c->n = 0;
+  c->seg_valid = false;
+  c->ctr_lo = c->ctr_hi = -1;
+  c->plan_G = 0;
   if (n > 0) {
     CUDA_TRY(cudaMemcpyAsync(c->w, w, bytes, cudaMemcpyDefault, c->stream));
     rc = reset_scalars(c, 0);
@@ -601,7 +793,7 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   if (ring && (ring_cap <= 0 || (ring_cap & (ring_cap - 1)) != 0))
     return fail(CLGEN_EINVAL, "stream_range: ring_cap must be a power of two");
   if (ring && !is_device_ptr(ring)) return fail(CLGEN_EINVAL, "stream_range: ring must be device memory");
-  if (stream_mode != CLGEN_STREAM_REFERENCE)
+  if (stream_mode != CLGEN_STREAM_REFERENCE && stream_mode != CLGEN_STREAM_COUNTER)
     return fail(CLGEN_EINVAL, "stream_range: unknown stream mode %d", stream_mode);
   if ((rc = set_device(c))) return rc;
   const int64_t ntracked = (c->n + (int64_t(1) << track_shift) - 1) >> track_shift;
@@ -613,14 +805,25 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   }
   if (degree && (!dev_deg || !accumulate) && ntracked > 0)
     CUDA_TRY(cudaMemsetAsync(d_deg, 0, ntracked * sizeof(uint32_t), c->stream));
-  if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
-  if (hi > lo) {
-    clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+  if (stream_mode == CLGEN_STREAM_COUNTER && hi > lo && S > 0.0) {
+    if ((rc = ensure_ctr_plan(c, S, lo, hi))) return rc;
+    if ((rc = reset_scalars(c, 0))) return rc;
+    clg::CtrWalkArgs a = ctr_args(c, S, lo, hi, seed);
     a.degree = d_deg;
     a.track_shift = track_shift;
     a.ring = reinterpret_cast<uint2*>(ring);
     a.ring_mask = ring ? static_cast<unsigned long long>(ring_cap - 1) : 0ull;
-    if ((rc = launch_walk<clg::kWalkFold>(c, a))) return rc;
+    if ((rc = launch_ctr<clg::kWalkFold>(c, a))) return rc;
+  } else {
+    if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
+    if (hi > lo && stream_mode == CLGEN_STREAM_REFERENCE) {
+      clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+      a.degree = d_deg;
+      a.track_shift = track_shift;
+      a.ring = reinterpret_cast<uint2*>(ring);
+      a.ring_mask = ring ? static_cast<unsigned long long>(ring_cap - 1) : 0ull;
+      if ((rc = launch_walk<clg::kWalkFold>(c, a))) return rc;
+    }
   }
   if (degree && !dev_deg && ntracked > 0)
     CUDA_TRY(cudaMemcpyAsync(degree, d_deg, ntracked * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
@@ -721,6 +924,39 @@ int clgen_dev_plan_ucp(clgen_dev_ctx* c, int P, int64_t* boundaries, double* cum
   b[P] = n;
   if (cum_costs && !is_device_ptr(cum_costs)) c->plan_G = 0;  // cum now holds finalized values
   CUDA_TRY(cudaMemcpy(boundaries, b.data(), b.size() * sizeof(long long), cudaMemcpyDefault));
+  return CLGEN_OK;
+}
+
+int clgen_dev_generate_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed,
+                             int stream_mode, uint32_t* pairs, int64_t cap, int64_t* count,
+                             int64_t* n_flagged) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  int rc = check_range(c, lo, hi);
+  if (rc) return rc;
+  if (stream_mode == CLGEN_STREAM_REFERENCE)
+    return materialise(c, S, lo, hi, nullptr, seed, pairs, cap, count, n_flagged);
+  if (stream_mode != CLGEN_STREAM_COUNTER) return fail(CLGEN_EINVAL, "generate_range: unknown stream mode %d", stream_mode);
+  if (n_flagged) *n_flagged = 0;
+  c->last_flagged = 0;
+  return materialise_ctr(c, S, lo, hi, seed, pairs, cap, count);
+}
+
+int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double split_cap) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (!(class_eps > 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be in (0,1]");
+  if (!(split_cap >= 32.0)) return fail(CLGEN_EINVAL, "split_cap must be >= 32");
+  c->seg_eps = class_eps;
+  c->split_cap = split_cap;
+  c->seg_valid = false;
+  c->ctr_lo = c->ctr_hi = -1;
+  return CLGEN_OK;
+}
+
+int clgen_dev_counter_plan_info(clgen_dev_ctx* c, int* classes, int64_t* hubs, int64_t* units) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (classes) *classes = c->seg_valid ? c->seg_K : 0;
+  if (hubs) *hubs = c->ctr_H;
+  if (units) *units = c->ctr_units;
   return CLGEN_OK;
 }
 

@@ -1,0 +1,442 @@
+// Counter-stream Chung–Lu sampler (the north star's counter-based RNG keyed by
+// (seed, u, draw index)).  Statistically exact, not stream-identical to the
+// reference: every pair (u, v>u) appears independently with probability
+// min(w_u w_v / S, 1), the law of edges_from_source (edge_skip.cpp:20-46).
+//
+// Envelope construction.  The destination axis is cut into weight classes
+// ("segments") [c_k, c_{k+1}) inside which the sorted weights vary by at most
+// a factor (1+eps): w[c_k] <= (1+eps) * w[c_{k+1}-1].  Inside a segment a
+// source u proposes candidates as a Bernoulli(pbar) process with the CONSTANT
+// envelope pbar = min(w_u w[c_k] / S, 1) — i.i.d. geometric skips, so the skip
+// no longer depends on the previous candidate's weight — and thins each
+// candidate with probability q/pbar = w_v / w[c_k].  Since that ratio is at
+// least w[c_{k+1}-1]/w[c_k] >= 1/(1+eps), a candidate whose accept draw is
+// below it is accepted WITHOUT reading w[v]; only the remaining ~eps/2 of the
+// candidates gather their weight.  A skip past the segment end restarts at the
+// next segment (memorylessness).  Saturated segments (pbar = 1) propose every
+// position and accept with probability min(q, 1).
+//
+// Work units: (source u, v-range [lo,hi), split index s).  Heavy sources are
+// split into v-ranges of about kSplitCand expected candidates (level-2
+// balance, hub splitting) — a deterministic function of the weights, so the
+// edge set does not depend on the GPU count or the schedule.
+#pragma once
+
+#include "common.cuh"
+#include "sampler_ref.cuh"
+
+namespace clg {
+
+// ---- Philox4x32-10 (Salmon et al., SC'11) --------------------------------
+struct P4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ P4 philox4x32_10(P4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = P4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// 53-bit uniform strictly inside (0,1): (x>>11 + 1/2) * 2^-53.
+__device__ __forceinline__ double u53(uint32_t hi, uint32_t lo) {
+  const uint64_t x = (static_cast<uint64_t>(hi) << 32) | lo;
+  return __dmul_rn(static_cast<double>(x >> 11) + 0.5, 0x1.0p-53);
+}
+
+struct Segments {
+  const int64_t* start;  // K+1 entries, start[K] = n
+  const double* wfirst;  // w[start[k]]   (the class envelope)
+  const double* sure;    // w[start[k+1]-1] / w[start[k]]  (accept without gather below this)
+  int K;
+};
+
+struct CtrWalkArgs {
+  const double* __restrict__ w;
+  int64_t n;
+  double S;
+  int64_t lo, hi;          // source range [lo,hi)
+  uint32_t key0, key1;     // Philox key from the seed
+  Segments seg;
+  // hub splitting: sources [lo, lo+H) are split; unit prefix over them
+  int64_t H;
+  const int64_t* hub_units;  // H+1 prefix of split counts (hub_units[0] = 0)
+  int64_t total_units;       // hub_units[H] + (hi - lo - H)
+  unsigned long long* queue; // next unclaimed unit
+  // outputs (same meaning as RefWalkArgs)
+  int32_t* counts;           // per unit (count mode)
+  const int64_t* offsets;    // per unit (write mode)
+  uint2* pairs;
+  int64_t cap;
+  uint32_t* degree;
+  int track_shift;
+  uint2* ring;
+  unsigned long long ring_mask;
+  unsigned long long* ring_head;
+  unsigned long long* fold_out;
+  unsigned long long* overflow;
+};
+
+// Segment holding position j (binary search; K is small).
+__device__ __forceinline__ int seg_of(const Segments& s, int64_t j) {
+  int a = 0, b = s.K;  // start[a] <= j < start[b]
+  while (b - a > 1) {
+    const int m = (a + b) >> 1;
+    if (__ldg(s.start + m) <= j) a = m; else b = m;
+  }
+  return a;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos) {
+  constexpr int64_t kBatch = 32;
+  const int lane = lane_id();
+  const double* __restrict__ w = a.w;
+  const double S = a.S;
+
+  int64_t b_next = 0, b_end = 0;
+  bool drained = false;
+  unsigned long long r_next = 0, r_end = 0;
+
+  // lane state
+  int64_t unit = -1, u = 0, j = 0, vend = 0, seg_hi = 0, out_pos = 0;
+  int k = 0;
+  uint32_t d = 0, split = 0;
+  int32_t cnt = 0;
+  double wu = 0.0, wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
+  bool sat = false;
+  uint64_t checksum = 0;
+  unsigned long long edges_total = 0;
+
+  for (;;) {
+    const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
+    if (need && !drained) {
+      const int want = __popc(need);
+      const int r = __popc(need & lanemask_lt());
+      const bool me = (need >> lane) & 1u;
+      int64_t mine = -1;
+      const int64_t take1 = imin64(b_end - b_next, want);
+      if (me && r < take1) mine = b_next + r;
+      b_next += take1;
+      if (want > take1) {
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(a.queue, (unsigned long long)kBatch);
+        g = __shfl_sync(CLG_FULL, g, 0);
+        if (static_cast<int64_t>(g) >= a.total_units) {
+          drained = true;
+          b_next = b_end = a.total_units;
+        } else {
+          b_next = static_cast<int64_t>(g);
+          b_end = imin64(b_next + kBatch, a.total_units);
+          const int64_t take2 = imin64(b_end - b_next, want - take1);
+          if (me && r >= take1 && r - take1 < take2) mine = b_next + (r - take1);
+          b_next += take2;
+        }
+      }
+      if (mine >= 0) {
+        unit = mine;
+        // decode the unit
+        const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
+        if (mine < hub_units) {
+          int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
+          while (hi_h - lo_h > 1) {
+            const int64_t m = (lo_h + hi_h) >> 1;
+            if (a.hub_units[m] <= mine) lo_h = m; else hi_h = m;
+          }
+          u = a.lo + lo_h;
+          split = static_cast<uint32_t>(mine - a.hub_units[lo_h]);
+          j = split_pos[mine];
+          // the last split of a hub ends at n
+          vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
+        } else {
+          u = a.lo + a.H + (mine - hub_units);
+          split = 0;
+          j = u + 1;
+          vend = a.n;
+        }
+        d = 0;
+        cnt = 0;
+        if (MODE == kWalkWrite) out_pos = a.offsets[mine];
+        wu = w[u];
+        if (j < vend && S > 0.0 && wu > 0.0) {
+          k = seg_of(a.seg, j);
+          seg_hi = 0;  // force segment entry below
+        } else {
+          j = vend;  // nothing to do
+        }
+      }
+    }
+    const unsigned live = __ballot_sync(CLG_FULL, unit >= 0);
+    if (!live) {
+      if (drained) break;
+      continue;
+    }
+
+    bool accepted = false;
+    int64_t v = 0;
+    bool finish = false;
+    if (unit >= 0) {
+      if (j >= vend) {
+        finish = true;
+      } else {
+        if (j >= seg_hi) {
+          // enter the segment holding j
+          while (__ldg(a.seg.start + k + 1) <= j) ++k;
+          seg_hi = imin64(__ldg(a.seg.start + k + 1), vend);
+          wf = __ldg(a.seg.wfirst + k);
+          pb = __ddiv_rn(__dmul_rn(wu, wf), S);
+          sure = __ldg(a.seg.sure + k);
+          sat = pb >= 1.0;
+          if (!sat && pb > 0.0) ilp = __drcp_rn(log1p(-pb));
+        }
+        if (!(pb > 0.0)) {
+          finish = true;  // zero-weight tail: no further edges
+        } else {
+          const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
+                                      a.key0, a.key1);
+          ++d;
+          int64_t delta = 0;
+          bool over = false;
+          if (!sat) {
+            const double ratio = __dmul_rn(log(u53(rr.x, rr.y)), ilp);
+            if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
+            else delta = static_cast<int64_t>(ratio);
+          }
+          if (over) {
+            j = seg_hi;  // restart at the next segment (memoryless)
+          } else {
+            v = j + delta;
+            const double r2 = u53(rr.z, rr.w);
+            if (sat) {
+              const double q = __ddiv_rn(__dmul_rn(wu, w[v]), S);
+              accepted = q >= 1.0 || r2 < q;
+            } else {
+              accepted = r2 < sure || __dmul_rn(r2, wf) < w[v];
+            }
+            j = v + 1;
+          }
+        }
+      }
+    }
+
+    if (accepted) {
+      ++cnt;
+      if (MODE == kWalkWrite) {
+        if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
+        else atomicAdd(a.overflow, 1ull);
+        ++out_pos;
+      } else if (MODE == kWalkFold) {
+        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(v));
+        ++edges_total;
+        if (a.degree && (v & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
+      }
+    }
+    if (MODE == kWalkFold && a.ring) {
+      const unsigned am = __ballot_sync(CLG_FULL, accepted);
+      if (am) {
+        const unsigned kk = __popc(am);
+        const unsigned rk = __popc(am & lanemask_lt());
+        const unsigned long long rem = r_end - r_next;
+        unsigned long long nb = 0;
+        if (rem < kk) {
+          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);
+          nb = __shfl_sync(CLG_FULL, nb, 0);
+        }
+        if (accepted) {
+          const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);
+          a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
+        }
+        if (rem < kk) {
+          r_next = nb + (kk - rem);
+          r_end = nb + 2048ull;
+        } else {
+          r_next += kk;
+        }
+      }
+    }
+    if (unit >= 0 && (finish || j >= vend)) {
+      if (MODE == kWalkCount) a.counts[unit] = cnt;
+      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+      unit = -1;
+    }
+  }
+
+  if (MODE == kWalkFold) {
+    checksum = warp_sum_u64(checksum);
+    edges_total = warp_sum_u64(edges_total);
+    if (lane == 0) {
+      atomicAdd(&a.fold_out[0], edges_total);
+      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
+    }
+  }
+}
+
+// ---- segment table -------------------------------------------------------
+// Segment boundaries: c_0 = 0; c_{k+1} = first j > c_k with
+// w[j] * (1+eps) < w[c_k]  (or with w[j] == 0 when w[c_k] > 0).  One warp:
+// lanes probe 32 candidate positions per bisection round.
+__global__ void build_segments_kernel(const double* __restrict__ w, int64_t n, double eps, int kmax,
+                                      int64_t* start, double* wfirst, double* sure, int* K_out) {
+  const int lane = threadIdx.x;
+  int64_t c = 0;
+  int K = 0;
+  while (c < n && K < kmax) {
+    const double wc = w[c];
+    const double lim = wc > 0.0 ? wc / (1.0 + eps) : -1.0;  // next class: w < lim (zero class: never)
+    // first j in (c, n) with w[j] < lim, n if none; invariant: answer in (lo, hi]
+    int64_t lo = c, hi = n;
+    while (hi - lo > 1) {
+      const int64_t span = hi - lo - 1;
+      const int64_t step = (span + 31) / 32;
+      const int64_t p = lo + 1 + static_cast<int64_t>(lane) * step;
+      const bool below = p >= hi || w[p] < lim;
+      const unsigned m = __ballot_sync(CLG_FULL, below);
+      if (m == 0) {
+        lo = lo + 1 + 31 * step;
+        continue;
+      }
+      const int f = __ffs(m) - 1;
+      const int64_t pf = lo + 1 + static_cast<int64_t>(f) * step;
+      const int64_t nlo = f > 0 ? lo + 1 + static_cast<int64_t>(f - 1) * step : lo;
+      hi = pf < hi ? pf : hi;
+      lo = nlo;
+    }
+    if (lane == 0) {
+      start[K] = c;
+      wfirst[K] = wc;
+      const double wl = w[hi - 1];
+      sure[K] = wc > 0.0 ? wl / wc : 1.0;
+    }
+    ++K;
+    c = hi;
+  }
+  if (lane == 0) {
+    start[K] = n;
+    *K_out = (c < n) ? -1 : K;
+  }
+}
+
+// Hub split plan: for source u in [lo, lo+Hmax) the expected candidate count
+// over [u+1, n) under the segment envelope; split count = ceil(E / cap).
+__global__ void hub_splits_kernel(const double* __restrict__ w, int64_t n, double S, int64_t lo, int64_t Hmax,
+                                  Segments seg, const double* __restrict__ seg_mass, double cap,
+                                  int64_t* splits) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < Hmax; i += stride) {
+    const int64_t u = lo + i;
+    const double wu = w[u];
+    double E = 0.0;
+    if (u + 1 < n && wu > 0.0) {
+      int k = seg_of(seg, u + 1);
+      for (; k < seg.K; ++k) {
+        const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
+        const int64_t b = seg.start[k + 1];
+        if (b <= a) continue;
+        const double pb = wu * seg.wfirst[k] / S;
+        if (pb >= 1.0) E += static_cast<double>(b - a);
+        else E += wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
+      }
+    }
+    const double s = ceil(E / cap);
+    splits[i] = s < 1.0 ? 1 : static_cast<int64_t>(s);
+  }
+}
+
+// Split positions of every hub unit: split s of hub u covers
+// [pos(s), pos(s+1)) with pos chosen so each share carries E/splits expected
+// candidates (segment-level mass, positions interpolated inside a segment).
+__global__ void hub_positions_kernel(const double* __restrict__ w, int64_t n, double S, int64_t lo, int64_t H,
+                                     Segments seg, const double* __restrict__ seg_mass,
+                                     const int64_t* __restrict__ hub_units, int64_t* pos) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < H; i += stride) {
+    const int64_t u = lo + i;
+    const double wu = w[u];
+    const int64_t u0 = hub_units[i], ns = hub_units[i + 1] - u0;
+    // total expected candidates
+    const int k0 = seg_of(seg, u + 1);
+    double E = 0.0;
+    for (int k = k0; k < seg.K; ++k) {
+      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
+      const int64_t b = seg.start[k + 1];
+      if (b <= a) continue;
+      const double pb = wu * seg.wfirst[k] / S;
+      E += pb >= 1.0 ? static_cast<double>(b - a)
+                     : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
+    }
+    pos[u0] = u + 1;
+    int64_t s = 1;
+    double acc = 0.0;
+    for (int k = k0; k < seg.K && s < ns; ++k) {
+      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
+      const int64_t b = seg.start[k + 1];
+      if (b <= a) continue;
+      const double pb = wu * seg.wfirst[k] / S;
+      const double e = pb >= 1.0 ? static_cast<double>(b - a)
+                                 : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
+      while (s < ns && acc + e >= E * static_cast<double>(s) / static_cast<double>(ns)) {
+        const double frac = e > 0.0 ? (E * static_cast<double>(s) / static_cast<double>(ns) - acc) / e : 0.0;
+        int64_t p = a + static_cast<int64_t>(frac * static_cast<double>(b - a));
+        if (p < a) p = a;
+        if (p > b) p = b;
+        if (p <= pos[u0 + s - 1]) p = pos[u0 + s - 1];
+        pos[u0 + s] = p;
+        ++s;
+      }
+      acc += e;
+    }
+    for (; s < ns; ++s) pos[u0 + s] = n;
+  }
+}
+
+// seg_mass[k] = sum of w over segment k (any association; balance only).
+__global__ void segment_mass_kernel(const double* __restrict__ w, Segments seg, double* seg_mass) {
+  const int k = blockIdx.x;
+  if (k >= seg.K) return;
+  const int64_t a = seg.start[k], b = seg.start[k + 1];
+  double acc = 0.0;
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) acc += w[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CLG_FULL, acc, o);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+    seg_mass[k] = t;
+  }
+}
+
+// First index in [lo,hi) with w < lim (hi if none); w non-increasing.  One warp.
+__global__ void first_below_kernel(const double* __restrict__ w, int64_t lo0, int64_t hi0, double lim,
+                                   long long* out) {
+  const int lane = threadIdx.x;
+  int64_t lo = lo0 - 1, hi = hi0;  // answer in (lo, hi]
+  while (hi - lo > 1) {
+    const int64_t span = hi - lo - 1;
+    const int64_t step = (span + 31) / 32;
+    const int64_t p = lo + 1 + static_cast<int64_t>(lane) * step;
+    const bool below = p >= hi || w[p] < lim;
+    const unsigned m = __ballot_sync(CLG_FULL, below);
+    if (m == 0) {
+      lo = lo + 1 + 31 * step;
+      continue;
+    }
+    const int f = __ffs(m) - 1;
+    const int64_t pf = lo + 1 + static_cast<int64_t>(f) * step;
+    const int64_t nlo = f > 0 ? lo + 1 + static_cast<int64_t>(f - 1) * step : lo;
+    hi = pf < hi ? pf : hi;
+    lo = nlo;
+  }
+  if (lane == 0) *out = hi;
+}
+
+}  // namespace clg

@@ -1,0 +1,117 @@
+"""GPU tests of the counter-stream sampler: determinism, GPU-count/partition
+invariance, materialised == streamed, and the statistical law (per-pair
+frequencies vs min(w_u w_v / S, 1) at 5 sigma, the reference's convention in
+acceptance.cpp:80-124; degree chi^2 with exact FP64 expectations and a
+(chi^2 - k)/sqrt(2k) <= 5 tolerance, SURVEY.md §8(d) gate 3)."""
+import numpy as np
+import pytest
+
+import stats
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1406_1215_b200 import api as _api
+    return _api
+
+
+def canon_ok(e, n):
+    assert np.all(e[:, 0] < e[:, 1]) and np.all(e[:, 1] < n)
+    key = e[:, 0].astype(np.int64) * n + e[:, 1]
+    assert np.all(np.diff(key) > 0), "not strictly (u,v)-sorted / duplicates"
+
+
+def test_deterministic_sorted_unique(api, port):
+    w = port.synth_powerlaw(200_000, 2.1, 2.0, 2e4, 3)
+    ws = api.make_weight_sequence(w)
+    a = api.generate_range(ws, ws.sum_S, 0, w.size, 17)
+    b = api.generate_range(ws, ws.sum_S, 0, w.size, 17)
+    np.testing.assert_array_equal(a, b)
+    canon_ok(a, w.size)
+    c = api.generate_range(ws, ws.sum_S, 0, w.size, 18)
+    assert not np.array_equal(a[: min(len(a), len(c))], c[: min(len(a), len(c))])
+    info = ws.device.counter_plan_info()
+    assert info["classes"] > 10
+
+
+def test_streamed_equals_materialised_and_partition_invariant(api, port):
+    w = port.synth_powerlaw(300_000, 2.1, 2.0, 1e5, 9)  # inadmissible head, split hubs
+    ws = api.make_weight_sequence(w)
+    e = api.generate_range(ws, ws.sum_S, 0, w.size, 5)
+    full = api.stream_range(ws, ws.sum_S, 0, w.size, 5, mode="counter", track_shift=0)
+    assert full.count == len(e)
+    assert full.checksum == stats.checksum(e)
+    deg = np.bincount(e[:, 0], minlength=w.size) + np.bincount(e[:, 1], minlength=w.size)
+    np.testing.assert_array_equal(full.degree.astype(np.int64), deg)
+    assert ws.device.counter_plan_info()["hubs"] > 0
+    # any cover of the sources gives the same graph (UCP plans for 2, 4, 8 GPUs)
+    for G in (2, 4, 8):
+        b = api.plan_ucp(ws, G)
+        cnt, cks = 0, 0
+        for g in range(G):
+            r = api.stream_range(ws, ws.sum_S, int(b[g]), int(b[g + 1]), 5, mode="counter")
+            cnt += r.count
+            cks = (cks + r.checksum) % (1 << 64)
+        assert (cnt, cks) == (full.count, full.checksum), G
+
+
+def test_pair_frequencies_match_law(api):
+    # small instances incl. a clamped pair (w0 w1 / S >= 1) and zero weights
+    rng = np.random.default_rng(1)
+    cases = [np.array([4.0, 3.0, 2.0, 1.5, 1.0, 0.5, 0.0]),
+             np.sort(rng.uniform(0.2, 2.5, 12))[::-1].copy()]
+    trials = 20000
+    for w in cases:
+        ws = api.make_weight_sequence(w)
+        n = w.size
+        counts = np.zeros((n, n))
+        for t in range(trials):
+            e = api.generate_range(ws, ws.sum_S, 0, n, 1000 + t)
+            counts[e[:, 0], e[:, 1]] += 1
+        S = ws.sum_S
+        worst = 0.0
+        for u in range(n):
+            for v in range(u + 1, n):
+                p = min(w[u] * w[v] / S, 1.0)
+                sig = np.sqrt(p * (1 - p) / trials) + 1e-12
+                z = abs(counts[u, v] / trials - p) / sig
+                worst = max(worst, z)
+                if p in (0.0, 1.0):
+                    assert counts[u, v] == p * trials
+        assert worst < 5.0, worst
+
+
+@pytest.mark.parametrize("name,n,eps", [("c3", 1_000_000, 0.125), ("c5", 1_000_000, 0.125),
+                                        ("c3", 1_000_000, 0.5)])
+def test_degree_chi2(api, name, n, eps):
+    from paper_1406_1215_b200 import workloads
+    w = workloads.make(name, n)
+    ws = api.make_weight_sequence(w)
+    ws.device.set_counter_params(class_eps=eps, split_cap=1024.0)
+    res = api.stream_range(ws, ws.sum_S, 0, n, 2024, mode="counter", track_shift=0)
+    nodes = np.arange(n)
+    E, V = stats.expected_degrees(w, ws.sum_S, nodes)
+    z, k = stats.chi2_z(res.degree.astype(np.float64), E, V)
+    assert abs(z) <= 5.0, (z, k)
+    mean = E.sum() / 2
+    zt = (res.count - mean) / np.sqrt(V.sum() / 2)
+    assert abs(zt) <= 4.0, zt  # acceptance.cpp:268-271 total-edge convention
+
+
+def test_counter_vs_reference_same_law(api, port):
+    """Counter and reference streams agree in distribution (two-sample check on
+    total edges and per-bin degree counts over independent seeds)."""
+    w = port.synth_powerlaw(100_000, 2.5, 5.0, 300.0, 2)
+    ws = api.make_weight_sequence(w)
+    tot_c = [api.stream_range(ws, ws.sum_S, 0, w.size, s, mode="counter").count for s in range(20)]
+    tot_r = [api.stream_range(ws, ws.sum_S, 0, w.size, s, mode="reference").count for s in range(20)]
+    E, V = stats.expected_degrees(w, ws.sum_S, np.arange(w.size))
+    sd = np.sqrt(V.sum() / 2)
+    for t in tot_c + tot_r:
+        assert abs(t - E.sum() / 2) < 5 * sd
+    assert abs(np.mean(tot_c) - np.mean(tot_r)) < 5 * sd * np.sqrt(2 / 20)
