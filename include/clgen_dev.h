@@ -110,6 +110,11 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
  * w_last inside a class; default 1/8) and the hub split size in expected
  * candidates (default 4096).  Changing them changes the generated graph. */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);
+/* Reference stream arithmetic: 1 (default) = fast guarded FP64 (table log,
+ * series log1p, FMA-certified divisions; falls back to the reference
+ * expressions near rounding/floor boundaries, so results are identical);
+ * 0 = the reference expressions everywhere (validation). */
+int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
 /* Size of the last counter plan: weight classes, split sources, work units. */
 int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* hubs, int64_t* units);
 

@@ -140,6 +140,11 @@ class Device:
         """Counter-stream weight-class width and hub split size (changes the graph)."""
         check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, split_cap))
 
+    def set_fast_math(self, enable: bool = True) -> None:
+        """Reference-stream arithmetic: guarded fast path (default) or the
+        reference expressions everywhere; both give identical edges."""
+        check(_lib.lib().clgen_dev_set_fast_math(self._h, int(bool(enable))))
+
     def counter_plan_info(self) -> dict:
         k, h, u = C.c_int(), C.c_int64(), C.c_int64()
         check(_lib.lib().clgen_dev_counter_plan_info(self._h, C.byref(k), C.byref(h), C.byref(u)))

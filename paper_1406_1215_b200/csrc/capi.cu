@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 #include <string>
@@ -113,14 +114,16 @@ struct clgen_dev_ctx {
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
   // counter stream: weight-class segment table (per weights) and the hub
   // split plan of the last source range
-  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, hub_units, split_pos, unit_counts;
+  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   bool seg_valid = false;
   double seg_eps = 0.125;
   double split_cap = 4096.0;
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0;
   int ctr_blocks[3] = {0, 0, 0};
-  int walk_blocks[3] = {0, 0, 0};
+  int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  bool fast_math = true;
+  clg::LogTable* logtab = nullptr;  // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
   unsigned long long launches = 0;
@@ -152,22 +155,23 @@ int fetch_scalars(clgen_dev_ctx* c) {
   return CLGEN_OK;
 }
 
-template <int MODE>
+template <int MODE, bool FAST>
 int walk_grid(clgen_dev_ctx* c) {
-  if (!c->walk_blocks[MODE]) {
+  if (!c->walk_blocks[FAST][MODE]) {
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ref_walk_kernel<MODE>, 256, 0));
-    c->walk_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ref_walk_kernel<MODE, FAST>, 256, 0));
+    c->walk_blocks[FAST][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
   }
-  return c->walk_blocks[MODE];
+  return c->walk_blocks[FAST][MODE];
 }
 
 template <int MODE>
 int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a) {
-  const int grid = walk_grid<MODE>(c);
+  const int grid = c->fast_math ? walk_grid<MODE, true>(c) : walk_grid<MODE, false>(c);
   if (grid < 0) return grid;
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  clg::ref_walk_kernel<MODE><<<grid, 256, 0, c->stream>>>(a);
+  if (c->fast_math) clg::ref_walk_kernel<MODE, true><<<grid, 256, 0, c->stream>>>(a);
+  else clg::ref_walk_kernel<MODE, false><<<grid, 256, 0, c->stream>>>(a);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;
@@ -191,6 +195,8 @@ clg::RefWalkArgs walk_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   a.overflow = &c->sc->overflow;
   a.fold_out = c->sc->fold;
   a.ring_head = &c->sc->ring_head;
+  a.logtab = c->logtab;
+  a.invS = 1.0 / S;  // host IEEE division: RN(1/S)
   return a;
 }
 
@@ -353,13 +359,17 @@ int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, doubl
 }
 
 // ---- counter stream (sampler_ctr.cuh) ----------------------------------------
+clg::Segments segments(clgen_dev_ctx* c);
+
 int ensure_segments(clgen_dev_ctx* c) {
   if (c->seg_valid) return CLGEN_OK;
-  const int kmax = 4096;
+  const int kmax = clg::kSegSmemMax;
   CUDA_TRY(c->seg_start.ensure((kmax + 1) * sizeof(int64_t)));
   CUDA_TRY(c->seg_wfirst.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_sure.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_mass.ensure((kmax + 1) * sizeof(double)));
+  CUDA_TRY(c->seg_em.ensure((kmax + 1) * sizeof(double)));
+  CUDA_TRY(c->seg_invwf.ensure((kmax + 1) * sizeof(double)));
   double eps = c->seg_eps;
   for (int attempt = 0; attempt < 12; ++attempt, eps *= 2.0) {
     clg::build_segments_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, eps, kmax, c->seg_start.as<int64_t>(),
@@ -372,9 +382,11 @@ int ensure_segments(clgen_dev_ctx* c) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (K > 0) {
       c->seg_K = K;
-      clg::Segments sg{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(), K};
+      clg::Segments sg = segments(c);
+      sg.K = K;
       clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
-      ++c->launches;
+      clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>());
+      c->launches += 2;
       CUDA_TRY(cudaGetLastError());
       c->seg_valid = true;
       return CLGEN_OK;
@@ -384,7 +396,8 @@ int ensure_segments(clgen_dev_ctx* c) {
 }
 
 clg::Segments segments(clgen_dev_ctx* c) {
-  return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(), c->seg_K};
+  return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
+                       c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K};
 }
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected
@@ -605,9 +618,23 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       cudaMalloc(&c->sc, sizeof(Scalars)) != cudaSuccess ||
       cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
       cudaMalloc(&c->flagged, kFlagCap * sizeof(int64_t)) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess) {
     clgen_dev_destroy(c);
     return fail(CLGEN_ENOMEM, "clgen_dev_create: allocation failed");
+  }
+  {
+    // reciprocal centres and their logs, evaluated in long double on the host
+    clg::LogTable t;
+    for (int i = 0; i < clg::kLogTable; ++i) {
+      const long double ci = 1.0L + (static_cast<long double>(i) + 0.5L) / clg::kLogTable;
+      t.inv_c[i] = static_cast<double>(1.0L / ci);
+      t.nlog_inv[i] = static_cast<double>(-logl(static_cast<long double>(t.inv_c[i])));
+    }
+    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess) {
+      clgen_dev_destroy(c);
+      return fail(CLGEN_ECUDA, "clgen_dev_create: cannot upload log table");
+    }
   }
   *out = c;
   return CLGEN_OK;
@@ -621,6 +648,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (c->sc) cudaFree(c->sc);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->flagged) cudaFree(c->flagged);
+  if (c->logtab) cudaFree(c->logtab);
   c->counts.release();
   c->offsets.release();
   c->tiles.release();
@@ -635,6 +663,8 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->seg_wfirst.release();
   c->seg_sure.release();
   c->seg_mass.release();
+  c->seg_em.release();
+  c->seg_invwf.release();
   c->hub_units.release();
   c->split_pos.release();
   c->unit_counts.release();
@@ -949,6 +979,12 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double spli
   c->split_cap = split_cap;
   c->seg_valid = false;
   c->ctr_lo = c->ctr_hi = -1;
+  return CLGEN_OK;
+}
+
+int clgen_dev_set_fast_math(clgen_dev_ctx* c, int enable) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  c->fast_math = enable != 0;
   return CLGEN_OK;
 }
 

@@ -54,8 +54,13 @@ struct Segments {
   const int64_t* start;  // K+1 entries, start[K] = n
   const double* wfirst;  // w[start[k]]   (the class envelope)
   const double* sure;    // w[start[k+1]-1] / w[start[k]]  (accept without gather below this)
+  const double* em;      // K+1 envelope-mass prefix: em[k+1] = em[k] + wfirst[k] * len_k
+  const double* invwf;   // 1 / wfirst[k] (0 for a zero class)
   int K;
 };
+
+constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA
+constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
 
 struct CtrWalkArgs {
   const double* __restrict__ w;
@@ -83,7 +88,7 @@ struct CtrWalkArgs {
   unsigned long long* overflow;
 };
 
-// Segment holding position j (binary search; K is small).
+// Segment holding position j (binary search over start[]).
 __device__ __forceinline__ int seg_of(const Segments& s, int64_t j) {
   int a = 0, b = s.K;  // start[a] <= j < start[b]
   while (b - a > 1) {
@@ -93,9 +98,52 @@ __device__ __forceinline__ int seg_of(const Segments& s, int64_t j) {
   return a;
 }
 
+__device__ __forceinline__ double pbar_of(double wu, double wv, double S) {
+  return __ddiv_rn(__dmul_rn(wu, wv), S);  // the generators' q = w_u w_v / S
+}
+
+// First v in [a, b) with w_u w[v] / S < thr (b if none); monotone in v.
+__device__ __forceinline__ int64_t first_p_below(const double* __restrict__ w, double wu, double S, int64_t a,
+                                                 int64_t b, double thr) {
+  int64_t lo = a - 1, hi = b;  // answer in (lo, hi]
+  while (hi - lo > 1) {
+    const int64_t m = lo + ((hi - lo) >> 1);
+    if (pbar_of(wu, w[m], S) < thr) hi = m; else lo = m;
+  }
+  return hi;
+}
+
+enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
+
 template <int MODE>
 __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos) {
   constexpr int64_t kBatch = 32;
+  // class table in shared memory (falls back to global beyond kSegSmemMax)
+  __shared__ int64_t s_start[kSegSmemMax + 1];
+  __shared__ double s_em[kSegSmemMax + 1];
+  __shared__ double s_wf[kSegSmemMax];
+  __shared__ double s_iwf[kSegSmemMax];
+  __shared__ double s_sure[kSegSmemMax];
+  const int K = a.seg.K;
+  const bool smem = K <= kSegSmemMax;
+  if (smem) {
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+      s_start[i] = a.seg.start[i];
+      s_em[i] = a.seg.em[i];
+      if (i < K) {
+        s_wf[i] = a.seg.wfirst[i];
+        s_iwf[i] = a.seg.invwf[i];
+        s_sure[i] = a.seg.sure[i];
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t* __restrict__ g_start = smem ? s_start : a.seg.start;
+  const double* __restrict__ g_em = smem ? s_em : a.seg.em;
+  const double* __restrict__ g_wf = smem ? s_wf : a.seg.wfirst;
+  const double* __restrict__ g_iwf = smem ? s_iwf : a.seg.invwf;
+  const double* __restrict__ g_sure = smem ? s_sure : a.seg.sure;
+
   const int lane = lane_id();
   const double* __restrict__ w = a.w;
   const double S = a.S;
@@ -105,12 +153,12 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
   unsigned long long r_next = 0, r_end = 0;
 
   // lane state
-  int64_t unit = -1, u = 0, j = 0, vend = 0, seg_hi = 0, out_pos = 0;
-  int k = 0;
+  int64_t unit = -1, u = 0, j = 0, vend = 0, vsat = 0, vB = 0, seg_hi = 0, out_pos = 0;
+  int k = 0, phase = kPhHaz;
   uint32_t d = 0, split = 0;
   int32_t cnt = 0;
-  double wu = 0.0, wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
-  bool sat = false;
+  double wu = 0.0, c_u = 0.0, inv_c = 0.0, inv_kappa = 0.0, H = 0.0;
+  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;  // band phase
   uint64_t checksum = 0;
   unsigned long long edges_total = 0;
 
@@ -141,7 +189,6 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
       }
       if (mine >= 0) {
         unit = mine;
-        // decode the unit
         const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
         if (mine < hub_units) {
           int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
@@ -152,7 +199,6 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
           u = a.lo + lo_h;
           split = static_cast<uint32_t>(mine - a.hub_units[lo_h]);
           j = split_pos[mine];
-          // the last split of a hub ends at n
           vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
         } else {
           u = a.lo + a.H + (mine - hub_units);
@@ -165,10 +211,30 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
         if (MODE == kWalkWrite) out_pos = a.offsets[mine];
         wu = w[u];
         if (j < vend && S > 0.0 && wu > 0.0) {
-          k = seg_of(a.seg, j);
-          seg_hi = 0;  // force segment entry below
+          // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
+          const double y0 = pbar_of(wu, w[j], S);
+          if (y0 < kBandTau) {
+            vsat = vB = j;
+          } else {
+            vB = first_p_below(w, wu, S, j, vend, kBandTau);
+            vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
+          }
+          phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
+          seg_hi = 0;
+          if (vB < vend) {
+            k = seg_of(a.seg, vB);
+            // kappa from the class envelope holding vB (the largest pbar used)
+            const double ymax = pbar_of(wu, g_wf[k], S);
+            const double kappa = ymax > 0.0 ? __ddiv_rn(-log1p(-ymax), ymax) : 1.0;
+            c_u = __dmul_rn(kappa, __ddiv_rn(wu, S));
+            inv_c = __drcp_rn(c_u);
+            inv_kappa = __drcp_rn(kappa);
+            H = g_em[k] + g_wf[k] * static_cast<double>(vB - g_start[k]);
+            if (!(ymax > 0.0)) vend = vB;  // zero weights beyond vB
+          }
+          if (phase == kPhBand) k = seg_of(a.seg, j);
         } else {
-          j = vend;  // nothing to do
+          j = vend;
         }
       }
     }
@@ -184,43 +250,89 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
     if (unit >= 0) {
       if (j >= vend) {
         finish = true;
-      } else {
-        if (j >= seg_hi) {
-          // enter the segment holding j
-          while (__ldg(a.seg.start + k + 1) <= j) ++k;
-          seg_hi = imin64(__ldg(a.seg.start + k + 1), vend);
-          wf = __ldg(a.seg.wfirst + k);
-          pb = __ddiv_rn(__dmul_rn(wu, wf), S);
-          sure = __ldg(a.seg.sure + k);
-          sat = pb >= 1.0;
-          if (!sat && pb > 0.0) ilp = __drcp_rn(log1p(-pb));
-        }
-        if (!(pb > 0.0)) {
-          finish = true;  // zero-weight tail: no further edges
+      } else if (phase == kPhHaz) {
+        // ---- hazard envelope: Poisson(c_u * wfirst) proposals ------------
+        const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
+                                    a.key0, a.key1);
+        ++d;
+        const double T = H - log(u53(rr.x, rr.y)) * inv_c;
+        if (!(T < g_em[K])) {
+          finish = true;
         } else {
-          const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
-                                      a.key0, a.key1);
-          ++d;
-          int64_t delta = 0;
-          bool over = false;
-          if (!sat) {
-            const double ratio = __dmul_rn(log(u53(rr.x, rr.y)), ilp);
-            if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
-            else delta = static_cast<int64_t>(ratio);
-          }
-          if (over) {
-            j = seg_hi;  // restart at the next segment (memoryless)
-          } else {
-            v = j + delta;
-            const double r2 = u53(rr.z, rr.w);
-            if (sat) {
-              const double q = __ddiv_rn(__dmul_rn(wu, w[v]), S);
-              accepted = q >= 1.0 || r2 < q;
-            } else {
-              accepted = r2 < sure || __dmul_rn(r2, wf) < w[v];
+          if (!(T < g_em[k + 1])) {  // advance to the class holding T
+            int lo_k = k + 1, hi_k = K;  // em[lo_k] <= T < em[hi_k]
+            while (hi_k - lo_k > 1) {
+              const int m = (lo_k + hi_k) >> 1;
+              if (g_em[m] <= T) lo_k = m; else hi_k = m;
             }
-            j = v + 1;
+            k = lo_k;
           }
+          const int64_t s0 = g_start[k], s1 = g_start[k + 1];
+          const double iwf = g_iwf[k];
+          v = s0 + static_cast<int64_t>((T - g_em[k]) * iwf);
+          if (v < j) v = j;
+          if (v >= s1) v = s1 - 1;
+          if (v >= vend) {
+            finish = true;
+          } else {
+            // accept with q_v / (1 - e^{-z}), z = c_u wf: = (w_v/wf) * (1/kappa) * z/(1-e^{-z})
+            const double z = c_u * g_wf[k];
+            const double z2 = z * z;
+            const double bern = 1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
+                                z2 * z2 * z2 * (1.0 / 30240.0);
+            const double gfac = inv_kappa * bern;
+            const double r2 = u53(rr.z, rr.w);
+            accepted = r2 < g_sure[k] * gfac || r2 < gfac * (w[v] * iwf);
+            j = v + 1;
+            H = g_em[k] + g_wf[k] * static_cast<double>(j - s0);
+          }
+        }
+      } else if (phase == kPhSat) {
+        // ---- saturated band: q = 1, every position is an edge ------------
+        v = j;
+        accepted = true;
+        ++j;
+        if (j >= vsat) phase = vB > j ? kPhBand : kPhHaz;
+        if (phase == kPhBand) {
+          k = seg_of(a.seg, j);
+          seg_hi = 0;
+        }
+      } else {
+        // ---- heavy band: exact per-class geometric skips -----------------
+        if (j >= seg_hi) {
+          while (g_start[k + 1] <= j) ++k;
+          seg_hi = imin64(g_start[k + 1], vB);
+          wf = g_wf[k];
+          pb = fmin(pbar_of(wu, wf, S), 1.0);
+          sure = g_sure[k];
+          ilp = pb < 1.0 ? __drcp_rn(log1p(-pb)) : 0.0;
+        }
+        const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
+                                    a.key0, a.key1);
+        ++d;
+        int64_t delta = 0;
+        bool over = false;
+        if (pb < 1.0) {
+          const double ratio = __dmul_rn(log(u53(rr.x, rr.y)), ilp);
+          if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
+          else delta = static_cast<int64_t>(ratio);
+        }
+        if (over) {
+          j = seg_hi;
+        } else {
+          v = j + delta;
+          const double r2 = u53(rr.z, rr.w);
+          if (pb >= 1.0) {
+            const double q = pbar_of(wu, w[v], S);
+            accepted = q >= 1.0 || r2 < q;
+          } else {
+            accepted = r2 < sure || __dmul_rn(r2, wf) < w[v];
+          }
+          j = v + 1;
+        }
+        if (j >= vB) {
+          phase = kPhHaz;
+          if (vB < vend) k = seg_of(a.seg, vB);
         }
       }
     }
@@ -394,6 +506,19 @@ __global__ void hub_positions_kernel(const double* __restrict__ w, int64_t n, do
     }
     for (; s < ns; ++s) pos[u0 + s] = n;
   }
+}
+
+// Envelope-mass prefix em[k] and 1/wfirst (one thread; K is small).
+__global__ void segment_envelope_kernel(Segments seg, double* em, double* invwf) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (int k = 0; k < seg.K; ++k) {
+    em[k] = acc;
+    const double wf = seg.wfirst[k];
+    acc += wf * static_cast<double>(seg.start[k + 1] - seg.start[k]);
+    invwf[k] = wf > 0.0 ? 1.0 / wf : 0.0;
+  }
+  em[seg.K] = acc;
 }
 
 // seg_mass[k] = sum of w over segment k (any association; balance only).

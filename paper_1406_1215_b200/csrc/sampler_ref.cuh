@@ -9,6 +9,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace clg {
 
@@ -40,6 +41,9 @@ struct RefWalkArgs {
   int64_t* flagged;              // first flag_cap flagged source ids
   int64_t flag_cap;
   unsigned long long* overflow;  // write mode: slots beyond cap
+  // fast math (bit-exact with guarded fallbacks, fastmath.cuh)
+  const LogTable* logtab;
+  double invS;                   // RN(1/S)
 };
 
 // Skip length exactly as edge_skip.cpp:9-16 computes it, with CUDA's libm.
@@ -58,9 +62,30 @@ __device__ __forceinline__ int64_t skip_length_ref(double p, double r, bool& amb
   return static_cast<int64_t>(ratio);
 }
 
-template <int MODE>
+// Skip length with the fast guarded ratio; the exact reference expression
+// (and its glibc-vs-CUDA ambiguity flag) only inside a 2^-45 band around an
+// integer, where the fast ratio (error <= ~2^-48) cannot certify the floor.
+__device__ __forceinline__ int64_t skip_length_fast(double p, double r, bool& amb, const LogTable& T) {
+  const double ratio = log_fast(r, T) * __drcp_rn(log1m_fast(p, T));
+  const double fl = floor(ratio);
+  const double tol = ratio * 0x1p-45;
+  if (ratio < 1.0e18 && !((ratio - fl <= tol && fl >= 1.0) || (fl + 1.0) - ratio <= tol))
+    return static_cast<int64_t>(ratio);
+  return skip_length_ref(p, r, amb);
+}
+
+template <int MODE, bool FAST>
 __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   constexpr int64_t kBatch = 32;
+  __shared__ LogTable s_tab;
+  if (FAST) {
+    for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
+      s_tab.inv_c[i] = a.logtab->inv_c[i];
+      s_tab.nlog_inv[i] = a.logtab->nlog_inv[i];
+    }
+    __syncthreads();
+  }
+  const double invS = a.invS;
   const int lane = lane_id();
   const double* __restrict__ w = a.w;
   const int64_t n = a.n;
@@ -117,7 +142,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         if (MODE == kWalkWrite) out_pos = a.offsets[slot];
         if (j < n && S > 0.0) {
           rng.seed_key(node_rng_key(a.seed, u));
-          p = fmin(__ddiv_rn(__dmul_rn(wu, w[j]), S), 1.0);
+          p = fmin(FAST ? div_S(__dmul_rn(wu, w[j]), S, invS) : __ddiv_rn(__dmul_rn(wu, w[j]), S), 1.0);
         } else {
           p = 0.0;
         }
@@ -138,14 +163,15 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         finish = true;  // edge_skip.cpp:31 loop condition
       } else {
         int64_t delta = 0;
-        if (p < 1.0) delta = skip_length_ref(p, rng.open01(), amb);
+        if (p < 1.0) delta = FAST ? skip_length_fast(p, rng.open01(), amb, s_tab) : skip_length_ref(p, rng.open01(), amb);
         if (delta >= n - j) {
           finish = true;  // edge_skip.cpp:34
         } else {
           v = j + delta;
-          const double q = fmin(__ddiv_rn(__dmul_rn(wu, w[v]), S), 1.0);
+          const double prod = __dmul_rn(wu, w[v]);
+          const double q = fmin(FAST ? div_S(prod, S, invS) : __ddiv_rn(prod, S), 1.0);
           const double r2 = rng.open01();
-          accepted = r2 < __ddiv_rn(q, p);  // edge_skip.cpp:38
+          accepted = FAST ? accept_ref(r2, q, p) : r2 < __ddiv_rn(q, p);  // edge_skip.cpp:38
           p = q;
           j = v + 1;
         }

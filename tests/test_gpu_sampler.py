@@ -150,3 +150,29 @@ def mix64_np(z):
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         return z ^ (z >> np.uint64(31))
+
+
+def test_fast_math_identical_to_reference_expressions(api, port):
+    """The guarded fast FP64 path (table log, series log1p, certified
+    divisions) must reproduce the reference expressions bit for bit."""
+    rng = np.random.default_rng(2025)
+    cases = [port.synth_powerlaw(300_000, 2.5, 10.0, 1000.0, 1),      # C1 shape
+             np.full(200_000, 50.0),                                   # C2 shape
+             port.synth_powerlaw(200_000, 2.1, 2.0, 1e5, 2),           # saturated head
+             np.sort(rng.uniform(1e-3, 1.0, 100_000))[::-1].copy(),    # p ~ 1e-8 .. 1e-5
+             np.sort(rng.pareto(0.8, 50_000) + 1e-6)[::-1].copy()]     # extreme range
+    for i, w in enumerate(cases):
+        ws = api.make_weight_sequence(w)
+        seed = 1000 + i
+        ws.device.set_fast_math(True)
+        fast, f1 = api.serial_cl(ws, seed, return_flagged=True)
+        ws.device.set_fast_math(False)
+        slow, f2 = api.serial_cl(ws, seed, return_flagged=True)
+        np.testing.assert_array_equal(fast, slow, err_msg=f"case {i}")
+        assert f1 == f2 == 0
+        ws.device.set_fast_math(True)
+    # and against the oracle on the heaviest case
+    w = cases[2]
+    ws = api.make_weight_sequence(w)
+    exp, _, _, _ = port.create_edges_range(w, ws.sum_S, 0, w.size, 1002)
+    np.testing.assert_array_equal(api.serial_cl(ws, 1002), exp)
