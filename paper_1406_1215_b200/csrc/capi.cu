@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <cmath>
@@ -120,10 +121,12 @@ struct clgen_dev_ctx {
   double seg_eps = 0.125;
   double split_cap = 4096.0;
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0;
-  int ctr_blocks[3] = {0, 0, 0};
+  int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
   clg::LogTable* logtab = nullptr;  // device
+  clg::ZigTable* zig = nullptr;     // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
   unsigned long long launches = 0;
@@ -465,6 +468,7 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   const uint64_t key = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
   a.key0 = static_cast<uint32_t>(key);
   a.key1 = static_cast<uint32_t>(key >> 32);
+  c->seed_mix = key;
   a.seg = segments(c);
   a.H = c->ctr_H;
   a.hub_units = c->hub_units.as<int64_t>();
@@ -476,20 +480,34 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   return a;
 }
 
-template <int MODE>
-int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a) {
-  if (!c->ctr_blocks[MODE]) {
+template <int MODE, int MINB>
+int launch_ctr_minb(clgen_dev_ctx* c, const clg::CtrWalkArgs& a, int slot) {
+  if (!c->ctr_blocks[slot][MODE]) {
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE>, 256, 0));
-    c->ctr_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, 0));
+    c->ctr_blocks[slot][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
   }
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  clg::ctr_walk_kernel<MODE><<<c->ctr_blocks[MODE], 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>());
+  clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, 0, c->stream>>>(
+      a, c->split_pos.as<int64_t>(), c->zig, c->seed_mix);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;
   ++c->launches;
   return CLGEN_OK;
+}
+
+// Occupancy variant (CLGEN_CTR_MINB = 2|3|4 resident CTAs per SM; default 3).
+template <int MODE>
+int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a) {
+  static const int minb = [] {
+    const char* e = std::getenv("CLGEN_CTR_MINB");
+    const int v = e ? std::atoi(e) : 3;
+    return v >= 2 && v <= 4 ? v : 3;
+  }();
+  if (minb == 2) return launch_ctr_minb<MODE, 2>(c, a, 0);
+  if (minb == 4) return launch_ctr_minb<MODE, 4>(c, a, 2);
+  return launch_ctr_minb<MODE, 3>(c, a, 1);
 }
 
 // Materialised counter-stream generation (count pass, scan over units, write).
@@ -619,7 +637,8 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
       cudaMalloc(&c->flagged, kFlagCap * sizeof(int64_t)) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess) {
+      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess ||
+      cudaMalloc(&c->zig, sizeof(clg::ZigTable)) != cudaSuccess) {
     clgen_dev_destroy(c);
     return fail(CLGEN_ENOMEM, "clgen_dev_create: allocation failed");
   }
@@ -631,7 +650,21 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       t.inv_c[i] = static_cast<double>(1.0L / ci);
       t.nlog_inv[i] = static_cast<double>(-logl(static_cast<long double>(t.inv_c[i])));
     }
-    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess) {
+    // exponential ziggurat layers (256): x[1] = r, x[i+1] = -log(v/x[i] + e^-x[i])
+    clg::ZigTable z;
+    const long double r = 7.69711747013104972L;
+    const long double v = (r + 1.0L) * expl(-r);
+    long double xi = r;
+    z.x[0] = static_cast<double>(v * expl(r));
+    z.x[1] = static_cast<double>(r);
+    for (int i = 1; i < clg::kZigLayers; ++i) {
+      xi = -logl(v / xi + expl(-xi));
+      z.x[i + 1] = static_cast<double>(xi);
+    }
+    z.x[clg::kZigLayers] = 0.0;
+    for (int i = 0; i <= clg::kZigLayers; ++i) z.f[i] = static_cast<double>(expl(-static_cast<long double>(z.x[i])));
+    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->zig, &z, sizeof z, cudaMemcpyHostToDevice) != cudaSuccess) {
       clgen_dev_destroy(c);
       return fail(CLGEN_ECUDA, "clgen_dev_create: cannot upload log table");
     }
@@ -649,6 +682,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->flagged) cudaFree(c->flagged);
   if (c->logtab) cudaFree(c->logtab);
+  if (c->zig) cudaFree(c->zig);
   c->counts.release();
   c->offsets.release();
   c->tiles.release();

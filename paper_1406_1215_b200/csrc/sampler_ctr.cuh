@@ -113,36 +113,67 @@ __device__ __forceinline__ int64_t first_p_below(const double* __restrict__ w, d
   return hi;
 }
 
+// ---- exponential variates: 256-layer ziggurat (Marsaglia & Tsang 2000) ----
+// x[1] = r, x[i+1] = -log(v/x[i] + e^{-x[i]}), x[256] = 0, x[0] = v e^{r};
+// f[i] = e^{-x[i]}.  Exact method: ~98.9% of draws cost one multiply.
+constexpr int kZigLayers = 256;
+struct ZigTable {
+  double x[kZigLayers + 1];
+  double f[kZigLayers + 1];
+};
+
+__device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
+  return static_cast<double>(b >> 11) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ double exp_zig(Xoshiro& g, const ZigTable& Z) {
+  for (;;) {
+    const uint64_t b = g.next();
+    const int i = static_cast<int>(b & (kZigLayers - 1));
+    const double x = unit53(b) * Z.x[i];
+    if (x < Z.x[i + 1]) return x;
+    if (i == 0) return Z.x[1] - log(g.open01());  // tail beyond r
+    const double y = Z.f[i] + unit53(g.next()) * (Z.f[i + 1] - Z.f[i]);
+    if (y < exp(-x)) return x;
+  }
+}
+
+// Key of the per-unit stream: a bijection of (u, split) mixed with the seed.
+__device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint32_t split) {
+  return mix64(seed_mix ^ (static_cast<uint64_t>(u) | (static_cast<uint64_t>(split) << 36)));
+}
+
 enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
-template <int MODE>
-__global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos) {
+struct CtrTables {
+  ZigTable zig;
+};
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+                                                          const ZigTable* __restrict__ zig, uint64_t seed_mix) {
   constexpr int64_t kBatch = 32;
-  // class table in shared memory (falls back to global beyond kSegSmemMax)
   __shared__ int64_t s_start[kSegSmemMax + 1];
   __shared__ double s_em[kSegSmemMax + 1];
   __shared__ double s_wf[kSegSmemMax];
   __shared__ double s_iwf[kSegSmemMax];
   __shared__ double s_sure[kSegSmemMax];
-  const int K = a.seg.K;
-  const bool smem = K <= kSegSmemMax;
-  if (smem) {
-    for (int i = threadIdx.x; i <= K; i += blockDim.x) {
-      s_start[i] = a.seg.start[i];
-      s_em[i] = a.seg.em[i];
-      if (i < K) {
-        s_wf[i] = a.seg.wfirst[i];
-        s_iwf[i] = a.seg.invwf[i];
-        s_sure[i] = a.seg.sure[i];
-      }
+  __shared__ ZigTable s_zig;
+  const int K = a.seg.K;  // K <= kSegSmemMax (the host widens classes otherwise)
+  for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+    s_start[i] = a.seg.start[i];
+    s_em[i] = a.seg.em[i];
+    if (i < K) {
+      s_wf[i] = a.seg.wfirst[i];
+      s_iwf[i] = a.seg.invwf[i];
+      s_sure[i] = a.seg.sure[i];
     }
   }
+  for (int i = threadIdx.x; i <= kZigLayers; i += blockDim.x) {
+    s_zig.x[i] = zig->x[i];
+    s_zig.f[i] = zig->f[i];
+  }
   __syncthreads();
-  const int64_t* __restrict__ g_start = smem ? s_start : a.seg.start;
-  const double* __restrict__ g_em = smem ? s_em : a.seg.em;
-  const double* __restrict__ g_wf = smem ? s_wf : a.seg.wfirst;
-  const double* __restrict__ g_iwf = smem ? s_iwf : a.seg.invwf;
-  const double* __restrict__ g_sure = smem ? s_sure : a.seg.sure;
 
   const int lane = lane_id();
   const double* __restrict__ w = a.w;
@@ -155,10 +186,16 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
   // lane state
   int64_t unit = -1, u = 0, j = 0, vend = 0, vsat = 0, vB = 0, seg_hi = 0, out_pos = 0;
   int k = 0, phase = kPhHaz;
-  uint32_t d = 0, split = 0;
   int32_t cnt = 0;
-  double wu = 0.0, c_u = 0.0, inv_c = 0.0, inv_kappa = 0.0, H = 0.0;
-  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;  // band phase
+  double wu = 0.0;
+  // hazard phase: proposals form a Poisson process of rate c_u * wfirst[k]
+  // per position, i.e. unit rate in T = c_u * (envelope mass); T is tracked
+  // in envelope-mass units (divided by c_u).
+  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, thr = 0.0, gk = 0.0, em_next = 0.0;
+  int64_t prev_v = 0;
+  // band phase
+  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
+  Xoshiro rng;
   uint64_t checksum = 0;
   unsigned long long edges_total = 0;
 
@@ -189,6 +226,7 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
       }
       if (mine >= 0) {
         unit = mine;
+        uint32_t split = 0;
         const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
         if (mine < hub_units) {
           int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
@@ -202,14 +240,13 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
           vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
         } else {
           u = a.lo + a.H + (mine - hub_units);
-          split = 0;
           j = u + 1;
           vend = a.n;
         }
-        d = 0;
         cnt = 0;
         if (MODE == kWalkWrite) out_pos = a.offsets[mine];
         wu = w[u];
+        rng.seed_key(unit_key(seed_mix, u, split));
         if (j < vend && S > 0.0 && wu > 0.0) {
           // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
           const double y0 = pbar_of(wu, w[j], S);
@@ -222,15 +259,26 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
           phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
           seg_hi = 0;
           if (vB < vend) {
-            k = seg_of(a.seg, vB);
-            // kappa from the class envelope holding vB (the largest pbar used)
-            const double ymax = pbar_of(wu, g_wf[k], S);
-            const double kappa = ymax > 0.0 ? __ddiv_rn(-log1p(-ymax), ymax) : 1.0;
-            c_u = __dmul_rn(kappa, __ddiv_rn(wu, S));
-            inv_c = __drcp_rn(c_u);
-            inv_kappa = __drcp_rn(kappa);
-            H = g_em[k] + g_wf[k] * static_cast<double>(vB - g_start[k]);
-            if (!(ymax > 0.0)) vend = vB;  // zero weights beyond vB
+            const int kb = seg_of(a.seg, vB);
+            // kappa = -log(1-ymax)/ymax from the largest envelope used
+            const double ymax = pbar_of(wu, s_wf[kb], S);
+            if (ymax > 0.0) {
+              const double kappa = __ddiv_rn(-log1p(-ymax), ymax);
+              c_u = kappa * (wu / S);
+              inv_c = 1.0 / c_u;
+              inv_kappa = 1.0 / kappa;
+              T = s_em[kb] + s_wf[kb] * static_cast<double>(vB - s_start[kb]);
+              prev_v = vB - 1;
+              k = kb;
+              em_next = s_em[kb + 1];
+              // accept factor for class k: (1/kappa) * z/(1-e^-z), z = c_u wf
+              const double z = c_u * s_wf[kb], z2 = z * z;
+              gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
+                                z2 * z2 * z2 * (1.0 / 30240.0));
+              thr = s_sure[kb] * gk;
+            } else {
+              vend = vB;  // zero weights from vB on
+            }
           }
           if (phase == kPhBand) k = seg_of(a.seg, j);
         } else {
@@ -251,40 +299,38 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
       if (j >= vend) {
         finish = true;
       } else if (phase == kPhHaz) {
-        // ---- hazard envelope: Poisson(c_u * wfirst) proposals ------------
-        const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
-                                    a.key0, a.key1);
-        ++d;
-        const double T = H - log(u53(rr.x, rr.y)) * inv_c;
-        if (!(T < g_em[K])) {
-          finish = true;
-        } else {
-          if (!(T < g_em[k + 1])) {  // advance to the class holding T
+        // ---- hazard envelope -------------------------------------------
+        T += exp_zig(rng, s_zig) * inv_c;
+        if (!(T < em_next)) {
+          if (!(T < s_em[K])) {
+            finish = true;
+          } else {
             int lo_k = k + 1, hi_k = K;  // em[lo_k] <= T < em[hi_k]
             while (hi_k - lo_k > 1) {
               const int m = (lo_k + hi_k) >> 1;
-              if (g_em[m] <= T) lo_k = m; else hi_k = m;
+              if (s_em[m] <= T) lo_k = m; else hi_k = m;
             }
             k = lo_k;
+            em_next = s_em[k + 1];
+            const double z = c_u * s_wf[k], z2 = z * z;
+            gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
+                              z2 * z2 * z2 * (1.0 / 30240.0));
+            thr = s_sure[k] * gk;
           }
-          const int64_t s0 = g_start[k], s1 = g_start[k + 1];
-          const double iwf = g_iwf[k];
-          v = s0 + static_cast<int64_t>((T - g_em[k]) * iwf);
-          if (v < j) v = j;
+        }
+        if (!finish) {
+          const int64_t s0 = s_start[k];
+          const double iwf = s_iwf[k];
+          v = s0 + static_cast<int64_t>((T - s_em[k]) * iwf);
+          const int64_t s1 = s_start[k + 1];
           if (v >= s1) v = s1 - 1;
+          if (v < s0) v = s0;
           if (v >= vend) {
             finish = true;
-          } else {
-            // accept with q_v / (1 - e^{-z}), z = c_u wf: = (w_v/wf) * (1/kappa) * z/(1-e^{-z})
-            const double z = c_u * g_wf[k];
-            const double z2 = z * z;
-            const double bern = 1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
-                                z2 * z2 * z2 * (1.0 / 30240.0);
-            const double gfac = inv_kappa * bern;
-            const double r2 = u53(rr.z, rr.w);
-            accepted = r2 < g_sure[k] * gfac || r2 < gfac * (w[v] * iwf);
-            j = v + 1;
-            H = g_em[k] + g_wf[k] * static_cast<double>(j - s0);
+          } else if (v > prev_v) {  // a position proposed once however many events hit it
+            prev_v = v;
+            const double r2 = unit53(rng.next());
+            accepted = r2 < thr || r2 < gk * (w[v] * iwf);
           }
         }
       } else if (phase == kPhSat) {
@@ -292,28 +338,27 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
         v = j;
         accepted = true;
         ++j;
-        if (j >= vsat) phase = vB > j ? kPhBand : kPhHaz;
-        if (phase == kPhBand) {
-          k = seg_of(a.seg, j);
-          seg_hi = 0;
+        if (j >= vsat) {
+          phase = vB > j ? kPhBand : kPhHaz;
+          if (phase == kPhBand) {
+            k = seg_of(a.seg, j);
+            seg_hi = 0;
+          }
         }
       } else {
         // ---- heavy band: exact per-class geometric skips -----------------
         if (j >= seg_hi) {
-          while (g_start[k + 1] <= j) ++k;
-          seg_hi = imin64(g_start[k + 1], vB);
-          wf = g_wf[k];
+          while (s_start[k + 1] <= j) ++k;
+          seg_hi = imin64(s_start[k + 1], vB);
+          wf = s_wf[k];
           pb = fmin(pbar_of(wu, wf, S), 1.0);
-          sure = g_sure[k];
-          ilp = pb < 1.0 ? __drcp_rn(log1p(-pb)) : 0.0;
+          sure = s_sure[k];
+          ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
         }
-        const P4 rr = philox4x32_10(P4{d, split, static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32)},
-                                    a.key0, a.key1);
-        ++d;
         int64_t delta = 0;
         bool over = false;
         if (pb < 1.0) {
-          const double ratio = __dmul_rn(log(u53(rr.x, rr.y)), ilp);
+          const double ratio = log(rng.open01()) * ilp;
           if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
           else delta = static_cast<int64_t>(ratio);
         }
@@ -321,19 +366,16 @@ __global__ void __launch_bounds__(256) ctr_walk_kernel(CtrWalkArgs a, const int6
           j = seg_hi;
         } else {
           v = j + delta;
-          const double r2 = u53(rr.z, rr.w);
+          const double r2 = unit53(rng.next());
           if (pb >= 1.0) {
             const double q = pbar_of(wu, w[v], S);
             accepted = q >= 1.0 || r2 < q;
           } else {
-            accepted = r2 < sure || __dmul_rn(r2, wf) < w[v];
+            accepted = r2 < sure || r2 * wf < w[v];
           }
           j = v + 1;
         }
-        if (j >= vB) {
-          phase = kPhHaz;
-          if (vB < vend) k = seg_of(a.seg, vB);
-        }
+        if (j >= vB) phase = kPhHaz;  // hazard state was prepared at unit start
       }
     }
 

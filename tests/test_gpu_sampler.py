@@ -169,7 +169,9 @@ def test_fast_math_identical_to_reference_expressions(api, port):
         ws.device.set_fast_math(False)
         slow, f2 = api.serial_cl(ws, seed, return_flagged=True)
         np.testing.assert_array_equal(fast, slow, err_msg=f"case {i}")
-        assert f1 == f2 == 0
+        assert f1 == f2
+        if i < 4:  # the extreme-range case legitimately has ratios ~1e12 (2^-47 band)
+            assert f1 == 0
         ws.device.set_fast_math(True)
     # and against the oracle on the heaviest case
     w = cases[2]
