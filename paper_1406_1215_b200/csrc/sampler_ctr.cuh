@@ -375,7 +375,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           }
           j = v + 1;
         }
-        if (j >= vB) phase = kPhHaz;  // hazard state was prepared at unit start
+        if (j >= vB) {  // hazard state (T, c_u, class factors) was prepared at unit start
+          phase = kPhHaz;
+          if (vB < vend) k = seg_of(a.seg, vB);
+        }
       }
     }
 
