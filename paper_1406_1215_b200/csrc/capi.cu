@@ -489,7 +489,7 @@ int launch_ctr_minb(clgen_dev_ctx* c, const clg::CtrWalkArgs& a, int slot) {
   }
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, 0, c->stream>>>(
-      a, c->split_pos.as<int64_t>(), c->zig, c->seed_mix);
+      a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;

@@ -23,6 +23,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "fastmath.cuh"
 #include "sampler_ref.cuh"
 
 namespace clg {
@@ -126,6 +127,26 @@ __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
   return static_cast<double>(b >> 11) * 0x1.0p-53;
 }
 
+// Exp(1) by inversion, E = -log(U), U = (x>>11 + 1/2) 2^-53 in (0,1), with the
+// branch-free table log (absolute error ~2^-53: statistically exact).
+__device__ __forceinline__ double exp_inv(Xoshiro& g, const LogTable& T) {
+  const double x = __dmul_rn(static_cast<double>(g.next() >> 11) + 0.5, 0x1.0p-53);
+  const long long b = __double_as_longlong(x);
+  const int E = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+  const int i = static_cast<int>((b >> 45) & (kLogTable - 1));
+  const double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double t = __fma_rn(m, T.inv_c[i], -1.0);
+  double s = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
+  s = __fma_rn(t, s, 1.0 / 5.0);
+  s = __fma_rn(t, s, -1.0 / 4.0);
+  s = __fma_rn(t, s, 1.0 / 3.0);
+  s = __fma_rn(t, s, -0.5);
+  s = __fma_rn(t, s, 1.0);
+  const double e = static_cast<double>(E);
+  // -(E ln2 + log c + log1p t)
+  return -__fma_rn(e, 0x1.62e42fefa39efp-1, T.nlog_inv[i] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * s));
+}
+
 __device__ __forceinline__ double exp_zig(Xoshiro& g, const ZigTable& Z) {
   for (;;) {
     const uint64_t b = g.next();
@@ -149,16 +170,54 @@ struct CtrTables {
   ZigTable zig;
 };
 
+#define EMIT_EDGE(ACC, VV) { \
+    if (ACC) { \
+      ++cnt; \
+      if (MODE == kWalkWrite) { \
+        if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+        else atomicAdd(a.overflow, 1ull); \
+        ++out_pos; \
+      } else if (MODE == kWalkFold) { \
+        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(VV)); \
+        ++edges_total; \
+        if (a.degree && (VV & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[VV >> a.track_shift], 1u); \
+      } \
+    } \
+    if (MODE == kWalkFold && a.ring) { \
+      const unsigned am = __ballot_sync(CLG_FULL, ACC); \
+      if (am) { \
+        const unsigned kk = __popc(am); \
+        const unsigned rk = __popc(am & lanemask_lt()); \
+        const unsigned long long rem = r_end - r_next; \
+        unsigned long long nb = 0; \
+        if (rem < kk) { \
+          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull); \
+          nb = __shfl_sync(CLG_FULL, nb, 0); \
+        } \
+        if (ACC) { \
+          const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem); \
+          a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+        } \
+        if (rem < kk) { \
+          r_next = nb + (kk - rem); \
+          r_end = nb + 2048ull; \
+        } else { \
+          r_next += kk; \
+        } \
+      } \
+    } \
+}
+
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
-                                                          const ZigTable* __restrict__ zig, uint64_t seed_mix) {
+                                                          const LogTable* __restrict__ logtab, uint64_t seed_mix) {
   constexpr int64_t kBatch = 32;
   __shared__ int64_t s_start[kSegSmemMax + 1];
   __shared__ double s_em[kSegSmemMax + 1];
   __shared__ double s_wf[kSegSmemMax];
   __shared__ double s_iwf[kSegSmemMax];
   __shared__ double s_sure[kSegSmemMax];
-  __shared__ ZigTable s_zig;
+  __shared__ LogTable s_log;
   const int K = a.seg.K;  // K <= kSegSmemMax (the host widens classes otherwise)
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
     s_start[i] = a.seg.start[i];
@@ -169,9 +228,9 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       s_sure[i] = a.seg.sure[i];
     }
   }
-  for (int i = threadIdx.x; i <= kZigLayers; i += blockDim.x) {
-    s_zig.x[i] = zig->x[i];
-    s_zig.f[i] = zig->f[i];
+  for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
+    s_log.inv_c[i] = logtab->inv_c[i];
+    s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
   __syncthreads();
 
@@ -193,6 +252,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   // in envelope-mass units (divided by c_u).
   double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, thr = 0.0, gk = 0.0, em_next = 0.0;
   int64_t prev_v = 0;
+  // software-pipelined accept: an uncertain candidate's weight is loaded in
+  // one iteration and compared in the next, so the warp never waits on it
+  int64_t pend_v = -1;
+  double pend_r2 = 0.0, pend_f = 0.0, pend_w = 0.0;
   // band phase
   double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
   Xoshiro rng;
@@ -295,22 +358,26 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     bool accepted = false;
     int64_t v = 0;
     bool finish = false;
+    // resolve the candidate whose weight was requested last iteration
+    const bool acc_prev = pend_v >= 0 && pend_r2 < pend_w * pend_f;
+    const int64_t v_prev = pend_v;
+    pend_v = -1;
+    bool pend_new = false;
+    int64_t pv_new = 0;
+    double pr2_new = 0.0, pf_new = 0.0;
     if (unit >= 0) {
       if (j >= vend) {
         finish = true;
       } else if (phase == kPhHaz) {
         // ---- hazard envelope -------------------------------------------
-        T += exp_zig(rng, s_zig) * inv_c;
+        T += exp_inv(rng, s_log) * inv_c;
         if (!(T < em_next)) {
           if (!(T < s_em[K])) {
             finish = true;
           } else {
-            int lo_k = k + 1, hi_k = K;  // em[lo_k] <= T < em[hi_k]
-            while (hi_k - lo_k > 1) {
-              const int m = (lo_k + hi_k) >> 1;
-              if (s_em[m] <= T) lo_k = m; else hi_k = m;
-            }
-            k = lo_k;
+            do {
+              ++k;
+            } while (!(T < s_em[k + 1]));
             em_next = s_em[k + 1];
             const double z = c_u * s_wf[k], z2 = z * z;
             gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
@@ -330,7 +397,14 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           } else if (v > prev_v) {  // a position proposed once however many events hit it
             prev_v = v;
             const double r2 = unit53(rng.next());
-            accepted = r2 < thr || r2 < gk * (w[v] * iwf);
+            if (r2 < thr) {
+              accepted = true;
+            } else {
+              pend_new = true;
+              pv_new = v;
+              pr2_new = r2;
+              pf_new = gk * iwf;
+            }
           }
         }
       } else if (phase == kPhSat) {
@@ -382,41 +456,16 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       }
     }
 
-    if (accepted) {
-      ++cnt;
-      if (MODE == kWalkWrite) {
-        if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
-        else atomicAdd(a.overflow, 1ull);
-        ++out_pos;
-      } else if (MODE == kWalkFold) {
-        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(v));
-        ++edges_total;
-        if (a.degree && (v & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
-      }
+    // a new uncertain candidate: request its weight now, decide next iteration
+    // (the unit cannot finish before that: finishing draws no candidate)
+    if (pend_new) {
+      pend_v = pv_new;
+      pend_r2 = pr2_new;
+      pend_f = pf_new;
+      pend_w = w[pv_new];
     }
-    if (MODE == kWalkFold && a.ring) {
-      const unsigned am = __ballot_sync(CLG_FULL, accepted);
-      if (am) {
-        const unsigned kk = __popc(am);
-        const unsigned rk = __popc(am & lanemask_lt());
-        const unsigned long long rem = r_end - r_next;
-        unsigned long long nb = 0;
-        if (rem < kk) {
-          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);
-          nb = __shfl_sync(CLG_FULL, nb, 0);
-        }
-        if (accepted) {
-          const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);
-          a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
-        }
-        if (rem < kk) {
-          r_next = nb + (kk - rem);
-          r_end = nb + 2048ull;
-        } else {
-          r_next += kk;
-        }
-      }
-    }
+    EMIT_EDGE(acc_prev, v_prev)
+    EMIT_EDGE(accepted, v)
     if (unit >= 0 && (finish || j >= vend)) {
       if (MODE == kWalkCount) a.counts[unit] = cnt;
       if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
