@@ -115,8 +115,10 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double sp
  * expressions near rounding/floor boundaries, so results are identical);
  * 0 = the reference expressions everywhere (validation). */
 int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
-/* Size of the last counter plan: weight classes, split sources, work units. */
+/* Size of the last counter plan: weight classes, split sources, work units;
+ * and how many units (a prefix) run on the warp-cooperative kernel. */
 int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* hubs, int64_t* units);
+int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* ctx);
 
 /* Count pass only: per-source edge counts (int32, hi-lo entries, host or device). */
 int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,

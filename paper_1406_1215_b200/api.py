@@ -148,7 +148,8 @@ class Device:
     def counter_plan_info(self) -> dict:
         k, h, u = C.c_int(), C.c_int64(), C.c_int64()
         check(_lib.lib().clgen_dev_counter_plan_info(self._h, C.byref(k), C.byref(h), C.byref(u)))
-        return {"classes": k.value, "hubs": h.value, "units": u.value}
+        return {"classes": k.value, "hubs": h.value, "units": u.value,
+                "heavy_units": int(_lib.lib().clgen_dev_counter_heavy_units(self._h))}
 
     def flagged_nodes(self) -> np.ndarray:
         n = C.c_int64()

@@ -84,6 +84,7 @@ bool is_device_ptr(const void* ptr) {
 // Small per-call device scalars (one allocation, zeroed per call).
 struct Scalars {
   unsigned long long queue;
+  unsigned long long queue_heavy;
   unsigned long long ticket;
   unsigned long long flag_count;
   unsigned long long overflow;
@@ -120,8 +121,11 @@ struct clgen_dev_ctx {
   bool seg_valid = false;
   double seg_eps = 0.125;
   double split_cap = 4096.0;
-  int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0;
+  int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
+  double heavy_cand = 64.0;  // units with >= this many expected candidates run warp-cooperatively
+  DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  int ctr_warp_blocks[3] = {0, 0, 0};
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
@@ -452,6 +456,39 @@ int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
     CUDA_TRY(c->split_pos.ensure(sizeof(int64_t)));
   }
   c->ctr_units = hub_total + (hi - lo - (H > 0 ? H : 0));
+  // heavy plain sources: a prefix of [lo+H, hi) with expected candidates >=
+  // heavy_cand (the estimate is non-increasing in u); bracketed by sampling
+  // up to 1024 points per pass
+  {
+    const int64_t a0 = lo + (H > 0 ? H : 0);
+    int64_t lo_b = a0, hi_b = hi;  // answer (first light source) in [lo_b, hi_b]
+    const int mmax = 1024;
+    CUDA_TRY(c->probe.ensure(mmax * sizeof(double)));
+    std::vector<double> e(mmax);
+    while (hi_b > lo_b) {
+      const int64_t span = hi_b - lo_b;
+      const int m = static_cast<int>(span < mmax ? span : mmax);
+      clg::expected_candidates_kernel<<<(m + 255) / 256, 256, 0, c->stream>>>(
+          c->w, c->n, S, segments(c), c->seg_mass.as<double>(), lo_b, hi_b, m, c->probe.as<double>());
+      ++c->launches;
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(e.data(), c->probe.p, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      int i = 0;
+      while (i < m && e[i] >= c->heavy_cand) ++i;
+      auto ui = [&](int t) { return lo_b + span * t / m; };
+      if (i == m) {
+        lo_b = ui(m - 1) + 1;
+      } else if (i == 0) {
+        hi_b = lo_b;
+      } else {
+        const int64_t na = ui(i - 1) + 1, nb = ui(i);
+        lo_b = na;
+        hi_b = nb;
+      }
+    }
+    c->ctr_heavy = hub_total + (lo_b - a0);
+  }
   c->ctr_lo = lo;
   c->ctr_hi = hi;
   return CLGEN_OK;
@@ -481,33 +518,55 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
 }
 
 template <int MODE, int MINB>
-int launch_ctr_minb(clgen_dev_ctx* c, const clg::CtrWalkArgs& a, int slot) {
+int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a, int slot) {
   if (!c->ctr_blocks[slot][MODE]) {
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, 0));
     c->ctr_blocks[slot][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
   }
-  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, 0, c->stream>>>(
       a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
-  c->timed = true;
   ++c->launches;
   return CLGEN_OK;
 }
 
-// Occupancy variant (CLGEN_CTR_MINB = 2|3|4 resident CTAs per SM; default 3).
+// Heavy units (warp-cooperative kernel) then light units (lane-per-unit
+// kernel, occupancy variant CLGEN_CTR_MINB = 2|3|4, default 3).
 template <int MODE>
-int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a) {
+int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
   static const int minb = [] {
     const char* e = std::getenv("CLGEN_CTR_MINB");
     const int v = e ? std::atoi(e) : 3;
     return v >= 2 && v <= 4 ? v : 3;
   }();
-  if (minb == 2) return launch_ctr_minb<MODE, 2>(c, a, 0);
-  if (minb == 4) return launch_ctr_minb<MODE, 4>(c, a, 2);
-  return launch_ctr_minb<MODE, 3>(c, a, 1);
+  clg::CtrWalkArgs a = a_in;
+  const unsigned long long qstart[2] = {0ull, static_cast<unsigned long long>(c->ctr_heavy)};
+  CUDA_TRY(cudaMemcpyAsync(&c->sc->queue, &qstart[1], sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&c->sc->queue_heavy, &qstart[0], sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+  if (c->ctr_heavy > 0) {
+    if (!c->ctr_warp_blocks[MODE]) {
+      int per_sm = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE>, 256, 0));
+      c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    }
+    clg::ctr_warp_kernel<MODE><<<c->ctr_warp_blocks[MODE], 256, 0, c->stream>>>(
+        a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix, c->ctr_heavy, &c->sc->queue_heavy);
+    CUDA_TRY(cudaGetLastError());
+    ++c->launches;
+  }
+  if (c->ctr_units > c->ctr_heavy) {
+    int rc;
+    if (minb == 2) rc = launch_ctr_lane<MODE, 2>(c, a, 0);
+    else if (minb == 4) rc = launch_ctr_lane<MODE, 4>(c, a, 2);
+    else rc = launch_ctr_lane<MODE, 3>(c, a, 1);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  c->timed = true;
+  return CLGEN_OK;
 }
 
 // Materialised counter-stream generation (count pass, scan over units, write).
@@ -539,7 +598,6 @@ int materialise_ctr(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t
     d_pairs = c->pairs.as<uint2>();
     cap = stage;
   }
-  CUDA_TRY(cudaMemsetAsync(&c->sc->queue, 0, sizeof(unsigned long long), c->stream));
   a.counts = nullptr;
   a.offsets = c->offsets.as<int64_t>();
   a.pairs = d_pairs;
@@ -702,6 +760,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->hub_units.release();
   c->split_pos.release();
   c->unit_counts.release();
+  c->probe.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1015,6 +1074,8 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double spli
   c->ctr_lo = c->ctr_hi = -1;
   return CLGEN_OK;
 }
+
+int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* c) { return c ? c->ctr_heavy : -1; }
 
 int clgen_dev_set_fast_math(clgen_dev_ctx* c, int enable) {
   if (!c) return fail(CLGEN_EINVAL, "null context");

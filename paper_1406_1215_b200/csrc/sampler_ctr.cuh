@@ -484,6 +484,283 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   }
 }
 
+// ---- warp-cooperative processing of heavy units --------------------------
+// All 32 lanes work on one unit: round r, lane l takes Poisson event 32r+l of
+// the unit's hazard process (a warp prefix sum of exponentials), so positions
+// come out sorted across lanes; duplicates are adjacent (neighbour shuffle),
+// accepted edges are compacted by one ballot and stored contiguously.  Lane l
+// draws from its own keyed stream (unit key, lane), so the draws and hence
+// the edges are a deterministic function of (seed, u, split).
+__device__ __forceinline__ double warp_incl_scan_f64(double x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(CLG_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ double bern_gk(double inv_kappa, double z) {
+  const double z2 = z * z;
+  return inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) + z2 * z2 * z2 * (1.0 / 30240.0));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+                                                          const LogTable* __restrict__ logtab, uint64_t seed_mix,
+                                                          int64_t U_heavy, unsigned long long* queue_heavy) {
+  __shared__ int64_t s_start[kSegSmemMax + 1];
+  __shared__ double s_em[kSegSmemMax + 1];
+  __shared__ double s_wf[kSegSmemMax];
+  __shared__ double s_iwf[kSegSmemMax];
+  __shared__ double s_sure[kSegSmemMax];
+  __shared__ LogTable s_log;
+  const int K = a.seg.K;
+  for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+    s_start[i] = a.seg.start[i];
+    s_em[i] = a.seg.em[i];
+    if (i < K) {
+      s_wf[i] = a.seg.wfirst[i];
+      s_iwf[i] = a.seg.invwf[i];
+      s_sure[i] = a.seg.sure[i];
+    }
+  }
+  for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
+    s_log.inv_c[i] = logtab->inv_c[i];
+    s_log.nlog_inv[i] = logtab->nlog_inv[i];
+  }
+  __syncthreads();
+
+  const int lane = lane_id();
+  const unsigned lt_mask = lanemask_lt();
+  const double* __restrict__ w = a.w;
+  const double S = a.S;
+  const double em_end = s_em[K];
+  unsigned long long r_next = 0, r_end = 0;  // ring reservation (fold mode)
+  uint64_t checksum = 0;
+  unsigned long long edges_total = 0;
+  Xoshiro rng;
+
+  for (;;) {
+    unsigned long long ug = 0;
+    if (lane == 0) ug = atomicAdd(queue_heavy, 1ull);
+    const int64_t unit = static_cast<int64_t>(__shfl_sync(CLG_FULL, ug, 0));
+    if (unit >= U_heavy) break;
+    // ---- decode (warp-uniform) ----
+    int64_t u, j, vend;
+    uint32_t split = 0;
+    const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
+    if (unit < hub_units) {
+      int64_t lo_h = 0, hi_h = a.H;
+      while (hi_h - lo_h > 1) {
+        const int64_t m = (lo_h + hi_h) >> 1;
+        if (a.hub_units[m] <= unit) lo_h = m; else hi_h = m;
+      }
+      u = a.lo + lo_h;
+      split = static_cast<uint32_t>(unit - a.hub_units[lo_h]);
+      j = split_pos[unit];
+      vend = unit + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[unit + 1];
+    } else {
+      u = a.lo + a.H + (unit - hub_units);
+      j = u + 1;
+      vend = a.n;
+    }
+    const double wu = w[u];
+    int64_t out_pos = MODE == kWalkWrite ? a.offsets[unit] : 0;
+    int32_t cnt = 0;
+    // lane streams: key(u, split) mixed with the lane
+    rng.seed_key(mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1)));
+
+    // emit helper state per round: (acc, v) -> contiguous output
+#define WARP_EMIT(ACC, VV)                                                                              \
+  {                                                                                                     \
+    const unsigned am_ = __ballot_sync(CLG_FULL, ACC);                                                  \
+    if (am_) {                                                                                          \
+      const unsigned kk_ = __popc(am_);                                                                 \
+      const unsigned rk_ = __popc(am_ & lt_mask);                                                       \
+      if (MODE == kWalkWrite) {                                                                         \
+        if (ACC) {                                                                                      \
+          const int64_t pos_ = out_pos + rk_;                                                           \
+          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+          else atomicAdd(a.overflow, 1ull);                                                             \
+        }                                                                                               \
+        out_pos += kk_;                                                                                 \
+      } else if (MODE == kWalkFold) {                                                                   \
+        if (ACC) {                                                                                      \
+          checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(VV));              \
+          if (a.degree && ((VV) & ((1ll << a.track_shift) - 1)) == 0)                                   \
+            atomicAdd(&a.degree[(VV) >> a.track_shift], 1u);                                            \
+        }                                                                                               \
+        edges_total += (lane == 0) ? kk_ : 0;                                                           \
+        if (a.ring) {                                                                                   \
+          const unsigned long long rem_ = r_end - r_next;                                               \
+          unsigned long long nb_ = 0;                                                                   \
+          if (rem_ < kk_) {                                                                             \
+            if (lane == 0) nb_ = atomicAdd(a.ring_head, 2048ull);                                       \
+            nb_ = __shfl_sync(CLG_FULL, nb_, 0);                                                        \
+          }                                                                                             \
+          if (ACC) {                                                                                    \
+            const unsigned long long pos_ = rk_ < rem_ ? r_next + rk_ : nb_ + (rk_ - rem_);             \
+            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+          }                                                                                             \
+          if (rem_ < kk_) {                                                                             \
+            r_next = nb_ + (kk_ - rem_);                                                                \
+            r_end = nb_ + 2048ull;                                                                      \
+          } else {                                                                                      \
+            r_next += kk_;                                                                              \
+          }                                                                                             \
+        }                                                                                               \
+      }                                                                                                 \
+      cnt += kk_;                                                                                       \
+    }                                                                                                   \
+  }
+
+    if (j < vend && S > 0.0 && wu > 0.0) {
+      const double y0 = pbar_of(wu, w[j], S);
+      int64_t vB = j, vsat = j;
+      if (y0 >= kBandTau) {
+        vB = first_p_below(w, wu, S, j, vend, kBandTau);
+        vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
+      }
+      // ---- saturated band: every position is an edge (cooperative) ----
+      for (int64_t p0 = j; p0 < vsat; p0 += 32) {
+        const int64_t v = p0 + lane;
+        const bool acc = v < vsat;
+        WARP_EMIT(acc, v)
+      }
+      // ---- heavy band [vsat, vB): lane 0 walks exact per-class geometric skips ----
+      if (vsat < vB) {
+        int64_t jj = vsat;
+        int k = seg_of(a.seg, jj);
+        int64_t seg_hi = 0;
+        double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
+        while (jj < vB) {
+          bool acc = false;
+          int64_t v = 0;
+          if (lane == 0) {
+            if (jj >= seg_hi) {
+              while (s_start[k + 1] <= jj) ++k;
+              seg_hi = imin64(s_start[k + 1], vB);
+              wf = s_wf[k];
+              pb = fmin(pbar_of(wu, wf, S), 1.0);
+              sure = s_sure[k];
+              ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
+            }
+            int64_t delta = 0;
+            bool over = false;
+            if (pb < 1.0) {
+              const double ratio = log(rng.open01()) * ilp;
+              if (!(ratio < static_cast<double>(seg_hi - jj))) over = true;
+              else delta = static_cast<int64_t>(ratio);
+            }
+            if (over) {
+              jj = seg_hi;
+            } else {
+              v = jj + delta;
+              const double r2 = unit53(rng.next());
+              if (pb >= 1.0) {
+                const double q = pbar_of(wu, w[v], S);
+                acc = q >= 1.0 || r2 < q;
+              } else {
+                acc = r2 < sure || r2 * wf < w[v];
+              }
+              jj = v + 1;
+            }
+          }
+          jj = __shfl_sync(CLG_FULL, jj, 0);
+          WARP_EMIT(acc, v)
+        }
+      }
+      // ---- hazard envelope [vB, vend), cooperative rounds ----
+      if (vB < vend) {
+        int k = seg_of(a.seg, vB);
+        const double ymax = pbar_of(wu, s_wf[k], S);
+        if (ymax > 0.0) {
+          const double kappa = __ddiv_rn(-log1p(-ymax), ymax);
+          const double c_u = kappa * (wu / S);
+          const double inv_c = 1.0 / c_u;
+          const double inv_kappa = 1.0 / kappa;
+          double T0 = s_em[k] + s_wf[k] * static_cast<double>(vB - s_start[k]);
+          int64_t prev_v = vB - 1;
+          double gk = bern_gk(inv_kappa, c_u * s_wf[k]);
+          for (;;) {
+            const double T = T0 + warp_incl_scan_f64(exp_inv(rng, s_log)) * inv_c;
+            const double r2 = unit53(rng.next());
+            int kl = k;
+            while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
+            bool valid = T < em_end;
+            int64_t v = s_start[kl] + static_cast<int64_t>((T - s_em[kl]) * s_iwf[kl]);
+            if (v >= s_start[kl + 1]) v = s_start[kl + 1] - 1;
+            if (v < s_start[kl]) v = s_start[kl];
+            valid = valid && v < vend;
+            int64_t vp = __shfl_up_sync(CLG_FULL, v, 1);
+            if (lane == 0) vp = prev_v;
+            const bool propose = valid && v > vp;
+            const double g = kl == k ? gk : bern_gk(inv_kappa, c_u * s_wf[kl]);
+            bool acc = false;
+            if (propose) acc = r2 < s_sure[kl] * g || r2 < g * (w[v] * s_iwf[kl]);
+            WARP_EMIT(acc, v)
+            // carry the last lane's event into the next round
+            const bool all_valid = __all_sync(CLG_FULL, valid);
+            if (!all_valid) break;
+            T0 = __shfl_sync(CLG_FULL, T, 31);
+            const int k31 = __shfl_sync(CLG_FULL, kl, 31);
+            prev_v = __shfl_sync(CLG_FULL, v, 31);
+            if (k31 != k) {
+              k = k31;
+              gk = bern_gk(inv_kappa, c_u * s_wf[k]);
+            }
+          }
+        }
+      }
+    }
+#undef WARP_EMIT
+    if (MODE == kWalkCount && lane == 0) a.counts[unit] = cnt;
+    if (MODE == kWalkFold && lane == 0 && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+      atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+  }
+
+  if (MODE == kWalkFold) {
+    checksum = warp_sum_u64(checksum);
+    edges_total = warp_sum_u64(edges_total);
+    if (lane == 0) {
+      atomicAdd(&a.fold_out[0], edges_total);
+      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
+    }
+  }
+}
+
+// Envelope-expected candidate count of source u over [u+1, n) (the same
+// estimate that sizes hub splits); non-increasing in u.
+__device__ __forceinline__ double expected_candidates(const double* __restrict__ w, int64_t n, double S,
+                                                      const Segments& seg, const double* __restrict__ seg_mass,
+                                                      int64_t u) {
+  const double wu = w[u];
+  double E = 0.0;
+  if (u + 1 < n && wu > 0.0) {
+    for (int k = seg_of(seg, u + 1); k < seg.K; ++k) {
+      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
+      const int64_t b = seg.start[k + 1];
+      if (b <= a) continue;
+      const double pb = wu * seg.wfirst[k] / S;
+      E += pb >= 1.0 ? static_cast<double>(b - a)
+                     : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
+    }
+  }
+  return E;
+}
+
+// out[i] = expected_candidates(us[i])
+__global__ void expected_candidates_kernel(const double* __restrict__ w, int64_t n, double S, Segments seg,
+                                           const double* __restrict__ seg_mass, int64_t lo, int64_t hi, int m,
+                                           double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t u = lo + (hi - lo) * static_cast<int64_t>(i) / m;
+  out[i] = expected_candidates(w, n, S, seg, seg_mass, u);
+}
+
 // ---- segment table -------------------------------------------------------
 // Segment boundaries: c_0 = 0; c_{k+1} = first j > c_k with
 // w[j] * (1+eps) < w[c_k]  (or with w[j] == 0 when w[c_k] > 0).  One warp:

@@ -115,3 +115,25 @@ def test_counter_vs_reference_same_law(api, port):
     for t in tot_c + tot_r:
         assert abs(t - E.sum() / 2) < 5 * sd
     assert abs(np.mean(tot_c) - np.mean(tot_r)) < 5 * sd * np.sqrt(2 / 20)
+
+
+def test_heavy_light_split_and_law(api, port):
+    """Both kernels (warp-cooperative heavy units, lane-per-unit light units)
+    run and the joint output keeps the law; heavy/light choice per source is
+    a function of the weights only, so partitions agree."""
+    from paper_1406_1215_b200 import workloads
+    w = workloads.make("c4", 400_000)
+    ws = api.make_weight_sequence(w)
+    full = api.stream_range(ws, ws.sum_S, 0, w.size, 99, mode="counter", track_shift=0)
+    info = ws.device.counter_plan_info()
+    assert 0 < info["heavy_units"] < info["units"]
+    E, V = stats.expected_degrees(w, ws.sum_S, np.arange(w.size))
+    z, k = stats.chi2_z(full.degree.astype(np.float64), E, V)
+    assert abs(z) <= 5.0, (z, k)
+    e = api.generate_range(ws, ws.sum_S, 0, w.size, 99)
+    assert len(e) == full.count and stats.checksum(e) == full.checksum
+    canon_ok(e, w.size)
+    b = api.plan_ucp(ws, 4)
+    tot = sum(api.stream_range(ws, ws.sum_S, int(b[g]), int(b[g + 1]), 99, mode="counter").count
+              for g in range(4))
+    assert tot == full.count
