@@ -38,7 +38,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n", type=int, default=None, help="override node count (testing only)")
-    ap.add_argument("--mode", default="reference", choices=["reference", "counter"])
+    ap.add_argument("--mode", default="counter", choices=["reference", "counter"],
+                    help="random stream of the streaming configs (materialised C1/C2 always "
+                         "use the bit-exact reference stream)")
     ap.add_argument("--track-shift", type=int, default=6)
     ap.add_argument("--ring-log2", type=int, default=28)
     ap.add_argument("--no-e2e", action="store_true")

@@ -1,0 +1,226 @@
+// clgen_b200.hpp — header-only C++ mirror of the reference generator API
+// (namespace clgen in /root/reference/proj/core/include/clgen/*.hpp) on top of
+// the C ABI in clgen_dev.h.  Same names, argument meaning and error
+// behaviour: contract violations throw clgen_b200::error exactly where the
+// reference throws clgen::error.  A maintainer switches a caller with
+//     #include "clgen_b200.hpp"
+//     namespace clgen = clgen_b200;
+// and links libclgen_b200.so.
+//
+//   reference (clgen::)                          here (clgen_b200::)
+//   WeightSequence          weights.hpp:14-20     WeightSequence (+ device context)
+//   make_weight_sequence    weights.hpp:44        make_weight_sequence
+//   blocked_sum             weights.hpp:36        blocked_sum
+//   expected_total_edges    weights.hpp:55        expected_total_edges (host, O(n))
+//   Edge/EdgeSink/EdgeVector/EdgeCounter  edge_skip.hpp:15-49   same
+//   create_edges            edge_skip.hpp:58-59   create_edges
+//   create_edges_range      edge_skip.hpp:60-61   create_edges_range
+//   serial_cl               edge_skip.hpp:63      serial_cl
+//   plan_ucp_oracle         partition.hpp:56      plan_ucp_oracle (device, bit-identical)
+//   PartitionPlan           partition.hpp:20-31   PartitionPlan (ucp fields)
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <numeric>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "clgen_dev.h"
+
+namespace clgen_b200 {
+
+using node_t = std::int64_t;
+
+struct error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc != CLGEN_OK) throw error(clgen_dev_last_error());
+}
+
+// One device context (CUDA device + stream + resident weights).
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    clgen_dev_ctx* c = nullptr;
+    check(clgen_dev_create(device, &c));
+    ctx_.reset(c);
+  }
+  clgen_dev_ctx* get() const { return ctx_.get(); }
+
+ private:
+  struct Del {
+    void operator()(clgen_dev_ctx* c) const { clgen_dev_destroy(c); }
+  };
+  std::unique_ptr<clgen_dev_ctx, Del> ctx_;
+};
+
+struct WeightSequence {
+  std::vector<double> weights;      // non-increasing
+  double sum_S = 0.0;               // blocked_sum(weights), computed on the device
+  std::vector<node_t> orig_labels;  // sorted position -> original input label
+  std::shared_ptr<Device> device;   // owns the device copy of the weights
+
+  node_t size() const { return static_cast<node_t>(weights.size()); }
+};
+
+enum class SortPolicy { require_sorted, sort_desc };
+
+// weights.cpp:32-55
+inline WeightSequence make_weight_sequence(std::vector<double> weights, SortPolicy policy,
+                                           int device = 0) {
+  WeightSequence ws;
+  ws.orig_labels.resize(weights.size());
+  std::iota(ws.orig_labels.begin(), ws.orig_labels.end(), node_t{0});
+  if (policy == SortPolicy::sort_desc) {
+    std::stable_sort(ws.orig_labels.begin(), ws.orig_labels.end(),
+                     [&](node_t a, node_t b) { return weights[a] > weights[b]; });
+    ws.weights.reserve(weights.size());
+    for (node_t label : ws.orig_labels) ws.weights.push_back(weights[label]);
+  } else {
+    ws.weights = std::move(weights);
+  }
+  ws.device = std::make_shared<Device>(device);
+  // the device validates order (throws "weights unsorted at position u")
+  check(clgen_dev_set_weights(ws.device->get(), ws.weights.data(), ws.size()));
+  check(clgen_dev_blocked_sum(ws.device->get(), &ws.sum_S));
+  return ws;
+}
+
+// weights.cpp:21-30 on the device (any sequence)
+inline double blocked_sum(std::span<const double> xs, int device = 0) {
+  Device d(device);
+  double s = 0.0;
+  check(clgen_dev_blocked_sum_array(d.get(), xs.data(), static_cast<int64_t>(xs.size()), &s));
+  return s;
+}
+
+// weights.cpp:155-162 (host: O(n) input statistics, not on the device path)
+inline double expected_total_edges(const WeightSequence& ws) {
+  if (ws.sum_S <= 0.0) return 0.0;
+  std::vector<double> sq;
+  sq.reserve(ws.weights.size());
+  for (double w : ws.weights) sq.push_back(w * w);
+  return (ws.sum_S * ws.sum_S - blocked_sum(sq)) / (2.0 * ws.sum_S);
+}
+
+// ---- edges (edge_skip.hpp:15-49) -------------------------------------------
+struct Edge {
+  node_t u = 0;
+  node_t v = 0;
+  friend bool operator==(const Edge&, const Edge&) = default;
+  friend auto operator<=>(const Edge&, const Edge&) = default;
+};
+
+class EdgeSink {
+ public:
+  virtual ~EdgeSink() = default;
+  void emit(const Edge& e) {
+    on_edge(e);
+    ++count_;
+  }
+  std::int64_t count() const { return count_; }
+
+ private:
+  virtual void on_edge(const Edge& e) = 0;
+  std::int64_t count_ = 0;
+};
+
+class EdgeVector final : public EdgeSink {
+ public:
+  std::vector<Edge> edges;
+
+ private:
+  void on_edge(const Edge& e) override { edges.push_back(e); }
+};
+
+class EdgeCounter final : public EdgeSink {
+ private:
+  void on_edge(const Edge&) override {}
+};
+
+namespace detail {
+// Materialise on the device (uint32 pairs, reference emission order), then
+// feed the sink edge by edge so EdgeSink::count() advances as in the
+// reference.  Returns the emitted count.
+template <class Gen>
+std::int64_t run(Gen&& gen, EdgeSink& sink) {
+  std::int64_t count = 0, flagged = 0;
+  int rc = gen(nullptr, 0, &count, &flagged);  // count pass sizes the buffer
+  if (rc != CLGEN_OK && rc != CLGEN_ERANGE) check(rc);
+  std::vector<std::uint32_t> pairs(static_cast<size_t>(2 * std::max<std::int64_t>(count, 1)));
+  if (count > 0) check(gen(pairs.data(), count, &count, &flagged));
+  for (std::int64_t i = 0; i < count; ++i) sink.emit(Edge{pairs[2 * i], pairs[2 * i + 1]});
+  return count;
+}
+}  // namespace detail
+
+// edge_skip.cpp:60-66
+inline std::int64_t create_edges_range(const WeightSequence& ws, double S, node_t lo, node_t hi,
+                                       std::uint64_t seed, EdgeSink& sink) {
+  return detail::run(
+      [&](std::uint32_t* p, std::int64_t cap, std::int64_t* cnt, std::int64_t* fl) {
+        return clgen_dev_create_edges_range(ws.device->get(), S, lo, hi, seed, p, cap, cnt, fl);
+      },
+      sink);
+}
+
+// edge_skip.cpp:50-58
+inline std::int64_t create_edges(const WeightSequence& ws, double S, std::span<const node_t> sources,
+                                 std::uint64_t seed, EdgeSink& sink) {
+  return detail::run(
+      [&](std::uint32_t* p, std::int64_t cap, std::int64_t* cnt, std::int64_t* fl) {
+        return clgen_dev_create_edges(ws.device->get(), S, sources.data(),
+                                      static_cast<int64_t>(sources.size()), seed, p, cap, cnt, fl);
+      },
+      sink);
+}
+
+// edge_skip.cpp:68-70
+inline std::int64_t serial_cl(const WeightSequence& ws, std::uint64_t seed, EdgeSink& sink) {
+  return create_edges_range(ws, ws.sum_S, 0, ws.size(), seed, sink);
+}
+
+// ---- partitions (partition.hpp:20-56) ---------------------------------------
+struct PartitionPlan {
+  int procs = 1;
+  node_t n = 0;
+  std::vector<node_t> boundaries;  // n_0..n_P
+  node_t partition_size(int i) const {
+    if (i < 0 || i >= procs) throw error("partition_size: bad partition index");
+    return boundaries[static_cast<size_t>(i) + 1] - boundaries[static_cast<size_t>(i)];
+  }
+};
+
+// partition.cpp:159-203, computed on the device, bit-identical.
+inline PartitionPlan plan_ucp_oracle(const WeightSequence& ws, int P) {
+  PartitionPlan plan;
+  plan.procs = P;
+  plan.n = ws.size();
+  plan.boundaries.assign(static_cast<size_t>(std::max(P, 0)) + 1, 0);
+  check(clgen_dev_plan_ucp(ws.device->get(), P, plan.boundaries.data(), nullptr));
+  return plan;
+}
+
+// ---- streaming fold (no reference counterpart) -------------------------------
+struct StreamFold {
+  std::int64_t edges = 0;
+  std::uint64_t checksum = 0;  // sum of mix64((u<<32)|v) mod 2^64
+  std::int64_t flagged = 0;
+};
+
+inline StreamFold stream_range(const WeightSequence& ws, double S, node_t lo, node_t hi,
+                               std::uint64_t seed, bool counter_stream = true) {
+  StreamFold f;
+  check(clgen_dev_stream_range(ws.device->get(), S, lo, hi, seed,
+                               counter_stream ? CLGEN_STREAM_COUNTER : CLGEN_STREAM_REFERENCE, 0,
+                               nullptr, 0, nullptr, 0, &f.edges, &f.checksum, &f.flagged));
+  return f;
+}
+
+}  // namespace clgen_b200

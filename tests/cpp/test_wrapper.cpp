@@ -1,0 +1,70 @@
+// C++ drop-in test: the reference's own call patterns (test_edge_skip.cpp,
+// test_partition.cpp) against the clgen_b200:: mirror.  Prints one line per
+// check and exits non-zero on failure.  Needs a GPU at run time.
+#include <cstdio>
+#include <vector>
+
+#include "clgen_b200.hpp"
+
+namespace clgen = clgen_b200;
+using namespace clgen;
+
+static int failures = 0;
+#define CHECK(x)                                                  \
+  do {                                                            \
+    if (!(x)) {                                                   \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #x);     \
+      ++failures;                                                 \
+    }                                                             \
+  } while (0)
+
+int main() {
+  // test_partition.cpp:134-144: (4,3,2,1), P=2 -> (0,1,4)
+  const auto ws = make_weight_sequence({4, 3, 2, 1}, SortPolicy::require_sorted);
+  CHECK(ws.sum_S == 10.0);
+  CHECK((plan_ucp_oracle(ws, 2).boundaries == std::vector<node_t>{0, 1, 4}));
+
+  // test_edge_skip.cpp:84-96: degenerate cases and contract errors
+  const auto four = make_weight_sequence({2, 2, 2, 2}, SortPolicy::require_sorted);
+  EdgeVector sink;
+  const std::vector<node_t> last{3};
+  CHECK(create_edges(four, four.sum_S, last, 1, sink) == 0);
+  bool threw = false;
+  try {
+    const std::vector<node_t> bad{99};
+    create_edges(four, four.sum_S, bad, 1, sink);
+  } catch (const error&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    make_weight_sequence({1, 2}, SortPolicy::require_sorted);
+  } catch (const error&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // sort_desc keeps labels (weights.cpp:41-46)
+  const auto sd = make_weight_sequence({1, 3, 2}, SortPolicy::sort_desc);
+  CHECK((sd.orig_labels == std::vector<node_t>{1, 2, 0}));
+
+  // serial_cl is deterministic, canonical, and equals any disjoint cover
+  std::vector<double> w(2000);
+  for (size_t i = 0; i < w.size(); ++i) w[i] = 5.0 - 4.0 * static_cast<double>(i) / w.size();
+  const auto big = make_weight_sequence(w, SortPolicy::require_sorted);
+  EdgeVector a, b, c;
+  serial_cl(big, 42, a);
+  serial_cl(big, 42, b);
+  CHECK(a.edges == b.edges);
+  CHECK(a.count() == static_cast<std::int64_t>(a.edges.size()));
+  create_edges_range(big, big.sum_S, 0, 700, 42, c);
+  create_edges_range(big, big.sum_S, 700, big.size(), 42, c);
+  CHECK(c.edges == a.edges);
+  for (const Edge& e : a.edges) CHECK(e.u < e.v && e.v < big.size());
+  const auto f = stream_range(big, big.sum_S, 0, big.size(), 42, false);
+  CHECK(f.edges == a.count());
+
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
