@@ -56,7 +56,7 @@ int clgen_dev_last_kernel_ms(clgen_dev_ctx* ctx, float* ms);
  * (weights.cpp:32-55).  `w` (host or device) must be non-increasing and
  * non-negative; violations return CLGEN_EINVAL with the reference's message
  * ("weights unsorted at position u").  The context keeps its own device copy.
- * `n` may be 0.  Node ids must fit uint32 (n <= 2^32).
+ * `n` may be 0.  Node ids must fit uint32 (n < 2^32).
  */
 int clgen_dev_set_weights(clgen_dev_ctx* ctx, const double* w, int64_t n);
 int64_t clgen_dev_num_nodes(clgen_dev_ctx* ctx);

@@ -788,7 +788,7 @@ int clgen_dev_synchronize(clgen_dev_ctx* c) {
 int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (n < 0) return fail(CLGEN_EINVAL, "set_weights: negative n");
-  if (n > (int64_t(1) << 32)) return fail(CLGEN_EINVAL, "set_weights: n exceeds uint32 node ids");
+  if (n >= (int64_t(1) << 32)) return fail(CLGEN_EINVAL, "set_weights: n exceeds uint32 node ids (n < 2^32)");
   if (n > 0 && !w) return fail(CLGEN_EINVAL, "set_weights: null weights");
   int rc = set_device(c);
   if (rc) return rc;

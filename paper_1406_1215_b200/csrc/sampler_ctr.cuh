@@ -507,7 +507,7 @@ __device__ __forceinline__ double bern_gk(double inv_kappa, double z) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+__global__ void __launch_bounds__(256, 3) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                           const LogTable* __restrict__ logtab, uint64_t seed_mix,
                                                           int64_t U_heavy, unsigned long long* queue_heavy) {
   __shared__ int64_t s_start[kSegSmemMax + 1];
@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(256, 2) ctr_warp_kernel(CtrWalkArgs a, const i
         }
       }
       // ---- hazard envelope [vB, vend), cooperative rounds ----
+      // Node ids are < 2^32 here (n <= 2^32 - 1, checked by set_weights).
       if (vB < vend) {
         int k = seg_of(a.seg, vB);
         const double ymax = pbar_of(wu, s_wf[k], S);
@@ -682,34 +683,57 @@ __global__ void __launch_bounds__(256, 2) ctr_warp_kernel(CtrWalkArgs a, const i
           const double inv_c = 1.0 / c_u;
           const double inv_kappa = 1.0 / kappa;
           double T0 = s_em[k] + s_wf[k] * static_cast<double>(vB - s_start[k]);
-          int64_t prev_v = vB - 1;
-          double gk = bern_gk(inv_kappa, c_u * s_wf[k]);
+          uint32_t prev_v = static_cast<uint32_t>(vB - 1);
+          const uint32_t vend32 = static_cast<uint32_t>(vend);
+          // lane i holds the acceptance factor of class kw + i
+          int kw = k;
+          double g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
           for (;;) {
-            const double T = T0 + warp_incl_scan_f64(exp_inv(rng, s_log)) * inv_c;
+            // Exp(1) by inversion with the shared log table
+            double E;
+            {
+              const double x = __dmul_rn(static_cast<double>(rng.next() >> 11) + 0.5, 0x1.0p-53);
+              const long long bx = __double_as_longlong(x);
+              const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
+              const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
+              const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+              const double t = __fma_rn(m, s_log.inv_c[ti], -1.0);
+              double sp = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
+              sp = __fma_rn(t, sp, 1.0 / 5.0);
+              sp = __fma_rn(t, sp, -1.0 / 4.0);
+              sp = __fma_rn(t, sp, 1.0 / 3.0);
+              sp = __fma_rn(t, sp, -0.5);
+              sp = __fma_rn(t, sp, 1.0);
+              const double e = static_cast<double>(ex);
+              E = -__fma_rn(e, 0x1.62e42fefa39efp-1, s_log.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
+            }
+            const double T = T0 + warp_incl_scan_f64(E) * inv_c;
             const double r2 = unit53(rng.next());
             int kl = k;
             while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
-            bool valid = T < em_end;
-            int64_t v = s_start[kl] + static_cast<int64_t>((T - s_em[kl]) * s_iwf[kl]);
-            if (v >= s_start[kl + 1]) v = s_start[kl + 1] - 1;
-            if (v < s_start[kl]) v = s_start[kl];
-            valid = valid && v < vend;
-            int64_t vp = __shfl_up_sync(CLG_FULL, v, 1);
+            const uint32_t s0 = static_cast<uint32_t>(s_start[kl]);
+            const uint32_t s1 = static_cast<uint32_t>(s_start[kl + 1]);
+            const double iwf = s_iwf[kl];
+            uint32_t v = s0 + static_cast<uint32_t>(fmax(T - s_em[kl], 0.0) * iwf);
+            if (v > s1 - 1) v = s1 - 1;
+            const bool valid = T < em_end && v < vend32;
+            uint32_t vp = __shfl_up_sync(CLG_FULL, v, 1);
             if (lane == 0) vp = prev_v;
             const bool propose = valid && v > vp;
-            const double g = kl == k ? gk : bern_gk(inv_kappa, c_u * s_wf[kl]);
+            const int di = kl - kw;
+            double g = __shfl_sync(CLG_FULL, g_lane, di & 31);
+            if (di >= 32) g = bern_gk(inv_kappa, c_u * s_wf[kl]);
             bool acc = false;
-            if (propose) acc = r2 < s_sure[kl] * g || r2 < g * (w[v] * s_iwf[kl]);
+            if (propose) acc = r2 < s_sure[kl] * g || r2 < g * (w[v] * iwf);
             WARP_EMIT(acc, v)
             // carry the last lane's event into the next round
-            const bool all_valid = __all_sync(CLG_FULL, valid);
-            if (!all_valid) break;
+            if (!__all_sync(CLG_FULL, valid)) break;
             T0 = __shfl_sync(CLG_FULL, T, 31);
-            const int k31 = __shfl_sync(CLG_FULL, kl, 31);
+            k = __shfl_sync(CLG_FULL, kl, 31);
             prev_v = __shfl_sync(CLG_FULL, v, 31);
-            if (k31 != k) {
-              k = k31;
-              gk = bern_gk(inv_kappa, c_u * s_wf[k]);
+            if (k - kw >= 16) {
+              kw = k;
+              g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
             }
           }
         }
