@@ -99,6 +99,11 @@ struct Scalars {
 
 constexpr int64_t kFlagCap = 4096;
 
+double env_double(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : dflt;
+}
+
 }  // namespace
 
 struct clgen_dev_ctx {
@@ -119,10 +124,10 @@ struct clgen_dev_ctx {
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   bool seg_valid = false;
-  double seg_eps = 0.125;
-  double split_cap = 4096.0;
+  double seg_eps = env_double("CLGEN_CTR_EPS", 0.125);
+  double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
-  double heavy_cand = 64.0;  // units with >= this many expected candidates run warp-cooperatively
+  double heavy_cand = env_double("CLGEN_CTR_HEAVY", 64.0);  // units with >= this many expected candidates run warp-cooperatively
   DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
@@ -547,13 +552,28 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
                            c->stream));
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   if (c->ctr_heavy > 0) {
+    static const int wminb = [] {
+      const char* e = std::getenv("CLGEN_WARP_MINB");
+      const int v = e ? std::atoi(e) : 3;
+      return v >= 2 && v <= 4 ? v : 3;
+    }();
     if (!c->ctr_warp_blocks[MODE]) {
       int per_sm = 0;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE>, 256, 0));
+      if (wminb == 2) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 2>, 256, 0));
+      else if (wminb == 4) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 4>, 256, 0));
+      else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 3>, 256, 0));
       c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
     }
-    clg::ctr_warp_kernel<MODE><<<c->ctr_warp_blocks[MODE], 256, 0, c->stream>>>(
-        a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix, c->ctr_heavy, &c->sc->queue_heavy);
+    const int g = c->ctr_warp_blocks[MODE];
+    if (wminb == 2)
+      clg::ctr_warp_kernel<MODE, 2><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
+                                                               c->ctr_heavy, &c->sc->queue_heavy);
+    else if (wminb == 4)
+      clg::ctr_warp_kernel<MODE, 4><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
+                                                               c->ctr_heavy, &c->sc->queue_heavy);
+    else
+      clg::ctr_warp_kernel<MODE, 3><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
+                                                               c->ctr_heavy, &c->sc->queue_heavy);
     CUDA_TRY(cudaGetLastError());
     ++c->launches;
   }

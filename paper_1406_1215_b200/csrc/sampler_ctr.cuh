@@ -506,8 +506,8 @@ __device__ __forceinline__ double bern_gk(double inv_kappa, double z) {
   return inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) + z2 * z2 * z2 * (1.0 / 30240.0));
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256, 3) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                           const LogTable* __restrict__ logtab, uint64_t seed_mix,
                                                           int64_t U_heavy, unsigned long long* queue_heavy) {
   __shared__ int64_t s_start[kSegSmemMax + 1];
