@@ -117,6 +117,8 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: map every rank to one GPU (multi-rank logic on a 1-GPU box, gloo)
+    local = int(os.environ.get("CLGEN_DEVICE_OVERRIDE", local))
     return ws, rank, local
 
 
@@ -194,7 +196,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("CLGEN_DIST_BACKEND", "nccl")  # gloo: multi-rank test on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     from paper_1406_1215_b200 import api, runtime, workloads
 
     wl = workloads.WORKLOADS[args.config]
@@ -272,9 +278,10 @@ def run_ours(args):
     ms_step = total_ms / args.steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms_step, kern_ms / args.steps], dtype=torch.float64, device="cuda")
+        cdev = runtime.comm_device(local)
+        t = torch.tensor([ms_step, kern_ms / args.steps], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e = torch.tensor([edges_total], dtype=torch.int64, device="cuda")
+        e = torch.tensor([edges_total], dtype=torch.int64, device=cdev)
         dist.all_reduce(e)
         ms_step, kern_step = float(t[0]), float(t[1])
         edges_all = int(e[0]) // args.steps

@@ -124,7 +124,7 @@ struct clgen_dev_ctx {
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   bool seg_valid = false;
-  double seg_eps = env_double("CLGEN_CTR_EPS", 0.125);
+  double seg_eps = env_double("CLGEN_CTR_EPS", 0.03125);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
   double heavy_cand = env_double("CLGEN_CTR_HEAVY", 64.0);  // units with >= this many expected candidates run warp-cooperatively
@@ -554,8 +554,8 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
   if (c->ctr_heavy > 0) {
     static const int wminb = [] {
       const char* e = std::getenv("CLGEN_WARP_MINB");
-      const int v = e ? std::atoi(e) : 3;
-      return v >= 2 && v <= 4 ? v : 3;
+      const int v = e ? std::atoi(e) : 4;
+      return v >= 2 && v <= 4 ? v : 4;
     }();
     if (!c->ctr_warp_blocks[MODE]) {
       int per_sm = 0;

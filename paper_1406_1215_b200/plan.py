@@ -125,6 +125,8 @@ def plan_ucp_collective(phases, n: int, S: float, G: int, g: int, comm) -> PlanR
 def plan_ucp_distributed(ws, world: int, rank: int) -> np.ndarray:
     """Rank `rank` of `world` GPU processes: the level-1 plan (NCCL)."""
     import torch
-    comm = TorchComm(device=torch.device("cuda", torch.cuda.current_device()))
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else None
+    comm = TorchComm(device=dev)
     res = plan_ucp_collective(DevicePhases(ws.device), ws.size(), ws.sum_S, world, rank, comm)
     return res.boundaries

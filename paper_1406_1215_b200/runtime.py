@@ -16,6 +16,13 @@ from . import api, workloads
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def comm_device(local: int):
+    """Tensor device for collectives: the GPU for NCCL, the host for gloo."""
+    import torch
+    import torch.distributed as dist
+    return torch.device(f"cuda:{local}") if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
 def shared_weights(config: str, n: int | None, world: int, rank: int, local: int) -> np.ndarray:
     """Rank 0 synthesises the workload's weights; the other ranks receive them
     over NCCL (every rank holds all of w)."""
@@ -23,14 +30,15 @@ def shared_weights(config: str, n: int | None, world: int, rank: int, local: int
         return workloads.make(config, n)
     import torch
     import torch.distributed as dist
-    meta = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+    dev = comm_device(local)
+    meta = torch.zeros(1, dtype=torch.int64, device=dev)
     w = None
     if rank == 0:
         w = workloads.make(config, n)
         meta[0] = w.size
     dist.broadcast(meta, 0)
-    t = (torch.from_numpy(w).to(f"cuda:{local}") if rank == 0
-         else torch.empty(int(meta[0]), dtype=torch.float64, device=f"cuda:{local}"))
+    t = (torch.from_numpy(w).to(dev) if rank == 0
+         else torch.empty(int(meta[0]), dtype=torch.float64, device=dev))
     dist.broadcast(t, 0)
     out = t.cpu().numpy() if rank != 0 else w
     del t
@@ -121,9 +129,9 @@ def e2e_measure(args, w_host: np.ndarray, world: int, rank: int, local: int, lo:
     e_step = edges // args.steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device=comm_device(local))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e = torch.tensor([e_step], dtype=torch.int64, device="cuda")
+        e = torch.tensor([e_step], dtype=torch.int64, device=comm_device(local))
         dist.all_reduce(e)
         ms, e_step = float(t[0]), int(e[0])
     dev.close()
