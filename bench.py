@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--n", type=int, default=None, help="override node count (testing only)")
+    ap.add_argument("--num-vertices", dest="n", type=int, default=None,
+                    help="override the node count (testing only)")
     ap.add_argument("--mode", default="counter", choices=["reference", "counter"],
                     help="random stream of the streaming configs (materialised C1/C2 always "
                          "use the bit-exact reference stream)")
