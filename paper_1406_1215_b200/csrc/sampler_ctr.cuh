@@ -688,7 +688,18 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
           // lane i holds the acceptance factor of class kw + i
           int kw = k;
           double g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
+          // count/fold modes resolve an uncertain accept one round later (its
+          // w[v] load overlaps the next round); the ordered write pass cannot
+          constexpr bool kDefer = MODE != kWalkWrite;
+          bool pend = false;
+          uint32_t pv = 0;
+          double pr2 = 0.0, pf = 0.0, pw = 0.0;
           for (;;) {
+            if (kDefer) {
+              const bool accp = pend && pr2 < pw * pf;
+              WARP_EMIT(accp, pv)
+              pend = false;
+            }
             // Exp(1) by inversion with the shared log table
             double E;
             {
@@ -724,10 +735,28 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             double g = __shfl_sync(CLG_FULL, g_lane, di & 31);
             if (di >= 32) g = bern_gk(inv_kappa, c_u * s_wf[kl]);
             bool acc = false;
-            if (propose) acc = r2 < s_sure[kl] * g || r2 < g * (w[v] * iwf);
+            if (propose) {
+              if (r2 < s_sure[kl] * g) {
+                acc = true;
+              } else if (kDefer) {
+                pend = true;
+                pv = v;
+                pr2 = r2;
+                pf = g * iwf;
+                pw = w[v];  // consumed next round
+              } else {
+                acc = r2 < g * (w[v] * iwf);
+              }
+            }
             WARP_EMIT(acc, v)
             // carry the last lane's event into the next round
-            if (!__all_sync(CLG_FULL, valid)) break;
+            if (!__all_sync(CLG_FULL, valid)) {
+              if (kDefer) {
+                const bool accp = pend && pr2 < pw * pf;
+                WARP_EMIT(accp, pv)
+              }
+              break;
+            }
             T0 = __shfl_sync(CLG_FULL, T, 31);
             k = __shfl_sync(CLG_FULL, kl, 31);
             prev_v = __shfl_sync(CLG_FULL, v, 31);
