@@ -710,6 +710,14 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
     return rc;
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  // Random 8-byte weight gathers: ask L2 not to over-fetch around a miss
+  // (CLGEN_L2_FETCH=32|64|128; 0 keeps the driver default).
+  {
+    const char* e = std::getenv("CLGEN_L2_FETCH");
+    const int g = e ? std::atoi(e) : 32;
+    if (g > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(g));
+    cudaGetLastError();
+  }
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&c->sc, sizeof(Scalars)) != cudaSuccess ||
       cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
@@ -841,6 +849,26 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
       return fail(CLGEN_EINVAL, "weights unsorted at position %llu", c->sc_host->first_bad);
   }
   c->n = n;
+  // Optional L2 persistence for the hot head of w (candidates land in
+  // proportion to w_v, and w is sorted descending): CLGEN_L2_PERSIST_MB.
+  {
+    const char* e = std::getenv("CLGEN_L2_PERSIST_MB");
+    const double mb = e ? std::atof(e) : 0.0;
+    if (mb > 0.0 && n > 0) {
+      size_t bytes = static_cast<size_t>(mb * 1048576.0);
+      if (bytes > static_cast<size_t>(n) * sizeof(double)) bytes = static_cast<size_t>(n) * sizeof(double);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+      cudaStreamAttrValue attr;
+      std::memset(&attr, 0, sizeof attr);
+      attr.accessPolicyWindow.base_ptr = c->w;
+      attr.accessPolicyWindow.num_bytes = bytes;
+      attr.accessPolicyWindow.hitRatio = 1.0f;
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+      cudaGetLastError();
+    }
+  }
   return CLGEN_OK;
 }
 
