@@ -9,6 +9,6 @@ python bench.py "$@" --no-e2e --no-cpu-baseline > gpurun_out/${tag}_plain.log 2>
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py "$@" --no-e2e --no-cpu-baseline \
     > gpurun_out/${tag}_ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:${kre} -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:${kre} -s ${NCU_SKIP:-1} -c 1 \
     -o gpurun_out/${tag} python bench.py "$@" --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_full.log 2>&1
 echo done
