@@ -275,8 +275,21 @@ def run_ours(args):
         torch.distributed.barrier()
     clk = clocks.stop()
 
+    # level-2 balance evidence: one extra untimed step with per-warp busy intervals
+    dev.set_warp_profile(True)
+    step()
+    wprof = dev.warp_profile()
+    dev.set_warp_profile(False)
+
     # max over ranks of the device time; sum of edges
     ms_step = total_ms / args.steps
+    per_gpu = [ms_step]
+    if world > 1:
+        import torch.distributed as dist
+        g = torch.zeros(world, dtype=torch.float64, device=runtime.comm_device(local))
+        mine = torch.tensor([ms_step], dtype=torch.float64, device=runtime.comm_device(local))
+        dist.all_gather_into_tensor(g, mine)
+        per_gpu = g.cpu().tolist()
     if world > 1:
         import torch.distributed as dist
         cdev = runtime.comm_device(local)
@@ -331,6 +344,12 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "load_balance": {
+                "warp_busy_max_over_mean": wprof["max_over_mean"],
+                "warp_busy_mean_ms": wprof["mean_ms"], "warp_busy_max_ms": wprof["max_ms"],
+                "kernel_span_ms": wprof["span_ms"], "warps": wprof["warps"],
+                "per_gpu_ms": per_gpu,
+                "per_gpu_max_over_mean": max(per_gpu) / (sum(per_gpu) / len(per_gpu))},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -131,6 +131,10 @@ struct clgen_dev_ctx {
   DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
+  // optional per-warp busy intervals of the sampler kernels
+  bool warp_prof = false;
+  DevBuf prof;
+  int prof_warps = 0;  // slots used by the last sampler launch(es)
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
@@ -148,6 +152,22 @@ namespace {
 int set_device(clgen_dev_ctx* c) {
   CUDA_TRY(cudaSetDevice(c->device));
   return CLGEN_OK;
+}
+
+// Per-warp profile slots for a launch of `grid` 256-thread CTAs.
+clg::WarpProf prof_slots(clgen_dev_ctx* c, int grid, bool first) {
+  clg::WarpProf p{nullptr, 0};
+  if (!c->warp_prof) return p;
+  if (first) c->prof_warps = 0;
+  const int warps = grid * 8;
+  if (c->prof.ensure(static_cast<size_t>(c->prof_warps + warps) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return p;
+  }
+  p.slots = c->prof.as<unsigned long long>();
+  p.base = c->prof_warps;
+  c->prof_warps += warps;
+  return p;
 }
 
 int reset_scalars(clgen_dev_ctx* c, unsigned long long queue_start) {
@@ -178,9 +198,11 @@ int walk_grid(clgen_dev_ctx* c) {
 }
 
 template <int MODE>
-int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a) {
+int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a_in) {
   const int grid = c->fast_math ? walk_grid<MODE, true>(c) : walk_grid<MODE, false>(c);
   if (grid < 0) return grid;
+  clg::RefWalkArgs a = a_in;
+  a.prof = prof_slots(c, grid, true);
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   if (c->fast_math) clg::ref_walk_kernel<MODE, true><<<grid, 256, 0, c->stream>>>(a);
   else clg::ref_walk_kernel<MODE, false><<<grid, 256, 0, c->stream>>>(a);
@@ -523,12 +545,14 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
 }
 
 template <int MODE, int MINB>
-int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a, int slot) {
+int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in, int slot) {
+  clg::CtrWalkArgs a = a_in;
   if (!c->ctr_blocks[slot][MODE]) {
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, 0));
     c->ctr_blocks[slot][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
   }
+  a.prof = prof_slots(c, c->ctr_blocks[slot][MODE], c->ctr_heavy == 0);
   clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, 0, c->stream>>>(
       a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix);
   CUDA_TRY(cudaGetLastError());
@@ -565,6 +589,7 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
       c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
     }
     const int g = c->ctr_warp_blocks[MODE];
+    a.prof = prof_slots(c, g, true);
     if (wminb == 2)
       clg::ctr_warp_kernel<MODE, 2><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
                                                                c->ctr_heavy, &c->sc->queue_heavy);
@@ -789,6 +814,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->split_pos.release();
   c->unit_counts.release();
   c->probe.release();
+  c->prof.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1124,6 +1150,42 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double spli
 }
 
 int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* c) { return c ? c->ctr_heavy : -1; }
+
+int clgen_dev_set_warp_profile(clgen_dev_ctx* c, int enable) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  c->warp_prof = enable != 0;
+  c->prof_warps = 0;
+  return CLGEN_OK;
+}
+
+int clgen_dev_warp_profile(clgen_dev_ctx* c, double* max_over_mean, double* mean_ms, double* max_ms,
+                           double* span_ms, int64_t* warps) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (!c->warp_prof || c->prof_warps == 0) return fail(CLGEN_EINVAL, "warp_profile: not enabled or no launch yet");
+  std::vector<unsigned long long> v(static_cast<size_t>(c->prof_warps) * 2);
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(v.data(), c->prof.p, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  double sum = 0.0, mx = 0.0;
+  unsigned long long t0 = ~0ull, t1 = 0;
+  int64_t k = 0;
+  for (int i = 0; i < c->prof_warps; ++i) {
+    const unsigned long long a = v[2 * i], b = v[2 * i + 1];
+    if (b <= a) continue;
+    const double d = static_cast<double>(b - a) * 1e-6;
+    sum += d;
+    mx = d > mx ? d : mx;
+    t0 = a < t0 ? a : t0;
+    t1 = b > t1 ? b : t1;
+    ++k;
+  }
+  const double mean = k ? sum / static_cast<double>(k) : 0.0;
+  if (max_over_mean) *max_over_mean = mean > 0.0 ? mx / mean : 1.0;
+  if (mean_ms) *mean_ms = mean;
+  if (max_ms) *max_ms = mx;
+  if (span_ms) *span_ms = k ? static_cast<double>(t1 - t0) * 1e-6 : 0.0;
+  if (warps) *warps = k;
+  return CLGEN_OK;
+}
 
 int clgen_dev_set_fast_math(clgen_dev_ctx* c, int enable) {
   if (!c) return fail(CLGEN_EINVAL, "null context");

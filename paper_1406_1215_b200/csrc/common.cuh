@@ -99,4 +99,21 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
   return x;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Optional per-warp busy interval: slots[2*gw] = start, slots[2*gw+1] = end
+// (ns, %globaltimer), gw = global warp id + base.  Used to report the
+// level-2 load balance (max/mean per-warp busy time).
+struct WarpProf {
+  unsigned long long* slots;
+  int base;
+  __device__ __forceinline__ int gw() const {
+    return base + static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  }
+};
+
 }  // namespace clg

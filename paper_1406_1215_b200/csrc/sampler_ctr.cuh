@@ -87,6 +87,7 @@ struct CtrWalkArgs {
   unsigned long long* ring_head;
   unsigned long long* fold_out;
   unsigned long long* overflow;
+  WarpProf prof;
 };
 
 // Segment holding position j (binary search over start[]).
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   __syncthreads();
 
   const int lane = lane_id();
+  const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const double* __restrict__ w = a.w;
   const double S = a.S;
 
@@ -474,6 +476,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     }
   }
 
+  if (a.prof.slots && lane == 0) {
+    const int g = a.prof.gw();
+    a.prof.slots[2 * g] = t_start;
+    a.prof.slots[2 * g + 1] = globaltimer_ns();
+  }
   if (MODE == kWalkFold) {
     checksum = warp_sum_u64(checksum);
     edges_total = warp_sum_u64(edges_total);
@@ -533,6 +540,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
   __syncthreads();
 
   const int lane = lane_id();
+  const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const unsigned lt_mask = lanemask_lt();
   const double* __restrict__ w = a.w;
   const double S = a.S;
@@ -774,6 +782,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
   }
 
+  if (a.prof.slots && lane == 0) {
+    const int g = a.prof.gw();
+    a.prof.slots[2 * g] = t_start;
+    a.prof.slots[2 * g + 1] = globaltimer_ns();
+  }
   if (MODE == kWalkFold) {
     checksum = warp_sum_u64(checksum);
     edges_total = warp_sum_u64(edges_total);

@@ -41,6 +41,7 @@ struct RefWalkArgs {
   int64_t* flagged;              // first flag_cap flagged source ids
   int64_t flag_cap;
   unsigned long long* overflow;  // write mode: slots beyond cap
+  WarpProf prof;                 // optional per-warp busy intervals
   // fast math (bit-exact with guarded fallbacks, fastmath.cuh)
   const LogTable* logtab;
   double invS;                   // RN(1/S)
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   }
   const double invS = a.invS;
   const int lane = lane_id();
+  const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const double* __restrict__ w = a.w;
   const int64_t n = a.n;
   const double S = a.S;
@@ -228,6 +230,11 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
     }
   }
 
+  if (a.prof.slots && lane == 0) {
+    const int g = a.prof.gw();
+    a.prof.slots[2 * g] = t_start;
+    a.prof.slots[2 * g + 1] = globaltimer_ns();
+  }
   if (MODE == kWalkFold) {
     checksum = warp_sum_u64(checksum);
     edges_total = warp_sum_u64(edges_total);
