@@ -345,9 +345,10 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "load_balance": {
-                "warp_busy_max_over_mean": wprof["max_over_mean"],
-                "warp_busy_mean_ms": wprof["mean_ms"], "warp_busy_max_ms": wprof["max_ms"],
-                "kernel_span_ms": wprof["span_ms"], "warps": wprof["warps"],
+                "per_launch_warp_busy": [
+                    {"max_over_mean": round(p["max_over_mean"], 4), "mean_ms": round(p["mean_ms"], 3),
+                     "max_ms": round(p["max_ms"], 3), "span_ms": round(p["span_ms"], 3),
+                     "warps": p["warps"]} for p in wprof],
                 "per_gpu_ms": per_gpu,
                 "per_gpu_max_over_mean": max(per_gpu) / (sum(per_gpu) / len(per_gpu))},
             "clocks": clk,

@@ -116,12 +116,14 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double sp
  * 0 = the reference expressions everywhere (validation). */
 int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
 /* Level-2 load-balance evidence: when enabled, the sampler kernels record
- * each warp's busy interval (%globaltimer); clgen_dev_warp_profile reports
- * max/mean per-warp busy time over the last generation call (all its
- * sampler launches), the mean and max in ms, the span first-start to
- * last-end, and the number of warps. */
+ * each warp's busy interval (%globaltimer).  For sampler launch `launch` of
+ * the last generation call (0 .. clgen_dev_warp_profile_launches()-1; the
+ * counter stream runs a heavy-unit and a light-unit kernel) report max/mean
+ * per-warp busy time, mean and max in ms, the span first-start to last-end,
+ * and the number of warps. */
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
-int clgen_dev_warp_profile(clgen_dev_ctx* ctx, double* max_over_mean, double* mean_ms,
+int clgen_dev_warp_profile_launches(clgen_dev_ctx* ctx);
+int clgen_dev_warp_profile(clgen_dev_ctx* ctx, int launch, double* max_over_mean, double* mean_ms,
                            double* max_ms, double* span_ms, int64_t* warps);
 /* Size of the last counter plan: weight classes, split sources, work units;
  * and how many units (a prefix) run on the warp-cooperative kernel. */

@@ -148,14 +148,19 @@ class Device:
     def set_warp_profile(self, enable: bool = True) -> None:
         check(_lib.lib().clgen_dev_set_warp_profile(self._h, int(bool(enable))))
 
-    def warp_profile(self) -> dict:
-        """max/mean per-warp busy time of the last generation call (level-2 balance)."""
-        r, mean, mx, span = C.c_double(), C.c_double(), C.c_double(), C.c_double()
-        k = C.c_int64()
-        check(_lib.lib().clgen_dev_warp_profile(self._h, C.byref(r), C.byref(mean), C.byref(mx),
-                                                C.byref(span), C.byref(k)))
-        return {"max_over_mean": r.value, "mean_ms": mean.value, "max_ms": mx.value,
-                "span_ms": span.value, "warps": k.value}
+    def warp_profile(self) -> list:
+        """Per sampler launch of the last generation call: max/mean per-warp busy
+        time (level-2 balance), mean/max ms, span ms, warps."""
+        L = _lib.lib()
+        out = []
+        for i in range(L.clgen_dev_warp_profile_launches(self._h)):
+            r, mean, mx, span = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+            k = C.c_int64()
+            check(L.clgen_dev_warp_profile(self._h, i, C.byref(r), C.byref(mean), C.byref(mx),
+                                           C.byref(span), C.byref(k)))
+            out.append({"max_over_mean": r.value, "mean_ms": mean.value, "max_ms": mx.value,
+                        "span_ms": span.value, "warps": k.value})
+        return out
 
     def counter_plan_info(self) -> dict:
         k, h, u = C.c_int(), C.c_int64(), C.c_int64()

@@ -135,6 +135,7 @@ struct clgen_dev_ctx {
   bool warp_prof = false;
   DevBuf prof;
   int prof_warps = 0;  // slots used by the last sampler launch(es)
+  std::vector<int> prof_launch;  // first slot of each of those launches
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
@@ -158,8 +159,12 @@ int set_device(clgen_dev_ctx* c) {
 clg::WarpProf prof_slots(clgen_dev_ctx* c, int grid, bool first) {
   clg::WarpProf p{nullptr, 0};
   if (!c->warp_prof) return p;
-  if (first) c->prof_warps = 0;
+  if (first) {
+    c->prof_warps = 0;
+    c->prof_launch.clear();
+  }
   const int warps = grid * 8;
+  c->prof_launch.push_back(c->prof_warps);
   if (c->prof.ensure(static_cast<size_t>(c->prof_warps + warps) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return p;
@@ -1158,17 +1163,21 @@ int clgen_dev_set_warp_profile(clgen_dev_ctx* c, int enable) {
   return CLGEN_OK;
 }
 
-int clgen_dev_warp_profile(clgen_dev_ctx* c, double* max_over_mean, double* mean_ms, double* max_ms,
-                           double* span_ms, int64_t* warps) {
+int clgen_dev_warp_profile(clgen_dev_ctx* c, int launch, double* max_over_mean, double* mean_ms,
+                           double* max_ms, double* span_ms, int64_t* warps) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (!c->warp_prof || c->prof_warps == 0) return fail(CLGEN_EINVAL, "warp_profile: not enabled or no launch yet");
-  std::vector<unsigned long long> v(static_cast<size_t>(c->prof_warps) * 2);
+  const int L = static_cast<int>(c->prof_launch.size());
+  if (launch < 0 || launch >= L) return fail(CLGEN_EINVAL, "warp_profile: launch %d of %d", launch, L);
+  const int lo = c->prof_launch[launch], hi = launch + 1 < L ? c->prof_launch[launch + 1] : c->prof_warps;
+  std::vector<unsigned long long> v(static_cast<size_t>(hi - lo) * 2);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(v.data(), c->prof.p, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(v.data(), c->prof.as<unsigned long long>() + 2 * lo, v.size() * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost));
   double sum = 0.0, mx = 0.0;
   unsigned long long t0 = ~0ull, t1 = 0;
   int64_t k = 0;
-  for (int i = 0; i < c->prof_warps; ++i) {
+  for (int i = 0; i < hi - lo; ++i) {
     const unsigned long long a = v[2 * i], b = v[2 * i + 1];
     if (b <= a) continue;
     const double d = static_cast<double>(b - a) * 1e-6;
@@ -1185,6 +1194,10 @@ int clgen_dev_warp_profile(clgen_dev_ctx* c, double* max_over_mean, double* mean
   if (span_ms) *span_ms = k ? static_cast<double>(t1 - t0) * 1e-6 : 0.0;
   if (warps) *warps = k;
   return CLGEN_OK;
+}
+
+int clgen_dev_warp_profile_launches(clgen_dev_ctx* c) {
+  return c && c->warp_prof ? static_cast<int>(c->prof_launch.size()) : 0;
 }
 
 int clgen_dev_set_fast_math(clgen_dev_ctx* c, int enable) {
