@@ -55,6 +55,20 @@ struct Xoshiro {
     return result;
   }
 
+  // xoshiro256+ output (s0 + s3) with the same state transition: used by the
+  // counter stream only (its top 53 bits are what the samplers consume).
+  __device__ __forceinline__ uint64_t next_plus() {
+    const uint64_t result = s0 + s3;
+    const uint64_t t = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= t;
+    s3 = rotl64(s3, 45);
+    return result;
+  }
+
   // rng.hpp:58-63: (x>>11)*2^-53, exact zeros rejected (loop taken with
   // probability 2^-53 per draw).
   __device__ __forceinline__ double open01() {

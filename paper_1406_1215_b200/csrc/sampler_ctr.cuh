@@ -100,6 +100,16 @@ __device__ __forceinline__ int seg_of(const Segments& s, int64_t j) {
   return a;
 }
 
+// Same as seg_of on a (shared-memory) copy of start[].
+__device__ __forceinline__ int seg_of_s(const int64_t* start, int K, int64_t j) {
+  int a = 0, b = K;
+  while (b - a > 1) {
+    const int m = (a + b) >> 1;
+    if (start[m] <= j) a = m; else b = m;
+  }
+  return a;
+}
+
 __device__ __forceinline__ double pbar_of(double wu, double wv, double S) {
   return __ddiv_rn(__dmul_rn(wu, wv), S);  // the generators' q = w_u w_v / S
 }
@@ -131,7 +141,7 @@ __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
 // Exp(1) by inversion, E = -log(U), U = (x>>11 + 1/2) 2^-53 in (0,1), with the
 // branch-free table log (absolute error ~2^-53: statistically exact).
 __device__ __forceinline__ double exp_inv(Xoshiro& g, const LogTable& T) {
-  const double x = __dmul_rn(static_cast<double>(g.next() >> 11) + 0.5, 0x1.0p-53);
+  const double x = __dmul_rn(static_cast<double>(g.next_plus() >> 11) + 0.5, 0x1.0p-53);
   const long long b = __double_as_longlong(x);
   const int E = static_cast<int>((b >> 52) & 0x7ff) - 1023;
   const int i = static_cast<int>((b >> 45) & (kLogTable - 1));
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
           seg_hi = 0;
           if (vB < vend) {
-            const int kb = seg_of(a.seg, vB);
+            const int kb = seg_of_s(s_start, K, vB);
             // kappa = -log(1-ymax)/ymax from the largest envelope used
             const double ymax = pbar_of(wu, s_wf[kb], S);
             if (ymax > 0.0) {
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
               vend = vB;  // zero weights from vB on
             }
           }
-          if (phase == kPhBand) k = seg_of(a.seg, j);
+          if (phase == kPhBand) k = seg_of_s(s_start, K, j);
         } else {
           j = vend;
         }
@@ -398,7 +408,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
             finish = true;
           } else if (v > prev_v) {  // a position proposed once however many events hit it
             prev_v = v;
-            const double r2 = unit53(rng.next());
+            const double r2 = unit53(rng.next_plus());
             if (r2 < thr) {
               accepted = true;
             } else {
@@ -417,7 +427,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         if (j >= vsat) {
           phase = vB > j ? kPhBand : kPhHaz;
           if (phase == kPhBand) {
-            k = seg_of(a.seg, j);
+            k = seg_of_s(s_start, K, j);
             seg_hi = 0;
           }
         }
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           j = seg_hi;
         } else {
           v = j + delta;
-          const double r2 = unit53(rng.next());
+          const double r2 = unit53(rng.next_plus());
           if (pb >= 1.0) {
             const double q = pbar_of(wu, w[v], S);
             accepted = q >= 1.0 || r2 < q;
@@ -453,7 +463,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         }
         if (j >= vB) {  // hazard state (T, c_u, class factors) was prepared at unit start
           phase = kPhHaz;
-          if (vB < vend) k = seg_of(a.seg, vB);
+          if (vB < vend) k = seg_of_s(s_start, K, vB);
         }
       }
     }
@@ -581,36 +591,53 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     rng.seed_key(mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1)));
 
     // emit helper state per round: (acc, v) -> contiguous output
-#define WARP_EMIT(ACC, VV)                                                                              \
+// Emit up to two edges per lane (A before B; A lanes before B lanes in the
+// output), one ballot pair and one ring reservation per call.
+#define WARP_EMIT2(ACCA, VA, ACCB, VB)                                                                   \
   {                                                                                                     \
-    const unsigned am_ = __ballot_sync(CLG_FULL, ACC);                                                  \
-    if (am_) {                                                                                          \
-      const unsigned kk_ = __popc(am_);                                                                 \
-      const unsigned rk_ = __popc(am_ & lt_mask);                                                       \
+    const unsigned ba_ = __ballot_sync(CLG_FULL, ACCA);                                                 \
+    const unsigned bb_ = __ballot_sync(CLG_FULL, ACCB);                                                 \
+    if (ba_ | bb_) {                                                                                    \
+      const unsigned ka_ = __popc(ba_);                                                                 \
+      const unsigned kk_ = ka_ + __popc(bb_);                                                           \
+      const unsigned ra_ = __popc(ba_ & lt_mask);                                                       \
+      const unsigned rb_ = ka_ + __popc(bb_ & lt_mask);                                                 \
       if (MODE == kWalkWrite) {                                                                         \
-        if (ACC) {                                                                                      \
-          const int64_t pos_ = out_pos + rk_;                                                           \
-          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+        if (ACCA) {                                                                                     \
+          const int64_t pos_ = out_pos + ra_;                                                           \
+          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VA)); \
+          else atomicAdd(a.overflow, 1ull);                                                             \
+        }                                                                                               \
+        if (ACCB) {                                                                                     \
+          const int64_t pos_ = out_pos + rb_;                                                           \
+          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VB)); \
           else atomicAdd(a.overflow, 1ull);                                                             \
         }                                                                                               \
         out_pos += kk_;                                                                                 \
       } else if (MODE == kWalkFold) {                                                                   \
-        if (ACC) {                                                                                      \
-          checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(VV));              \
-          if (a.degree && ((VV) & ((1ll << a.track_shift) - 1)) == 0)                                   \
-            atomicAdd(&a.degree[(VV) >> a.track_shift], 1u);                                            \
+        if (ACCA) {                                                                                     \
+          checksum += mix64(ukey | static_cast<uint64_t>(VA));                                          \
+          if (a.degree && ((VA) & tmask) == 0) atomicAdd(&a.degree[(VA) >> a.track_shift], 1u);        \
+        }                                                                                               \
+        if (ACCB) {                                                                                     \
+          checksum += mix64(ukey | static_cast<uint64_t>(VB));                                          \
+          if (a.degree && ((VB) & tmask) == 0) atomicAdd(&a.degree[(VB) >> a.track_shift], 1u);        \
         }                                                                                               \
         edges_total += (lane == 0) ? kk_ : 0;                                                           \
         if (a.ring) {                                                                                   \
-          const unsigned long long rem_ = r_end - r_next;                                               \
+          const unsigned rem_ = static_cast<unsigned>(r_end - r_next);                                  \
           unsigned long long nb_ = 0;                                                                   \
           if (rem_ < kk_) {                                                                             \
             if (lane == 0) nb_ = atomicAdd(a.ring_head, 2048ull);                                       \
             nb_ = __shfl_sync(CLG_FULL, nb_, 0);                                                        \
           }                                                                                             \
-          if (ACC) {                                                                                    \
-            const unsigned long long pos_ = rk_ < rem_ ? r_next + rk_ : nb_ + (rk_ - rem_);             \
-            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
+          if (ACCA) {                                                                                   \
+            const unsigned long long pos_ = ra_ < rem_ ? r_next + ra_ : nb_ + (ra_ - rem_);             \
+            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VA)); \
+          }                                                                                             \
+          if (ACCB) {                                                                                   \
+            const unsigned long long pos_ = rb_ < rem_ ? r_next + rb_ : nb_ + (rb_ - rem_);             \
+            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VB)); \
           }                                                                                             \
           if (rem_ < kk_) {                                                                             \
             r_next = nb_ + (kk_ - rem_);                                                                \
@@ -623,7 +650,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       cnt += kk_;                                                                                       \
     }                                                                                                   \
   }
+#define WARP_EMIT(ACC, VV) WARP_EMIT2(ACC, VV, false, 0u)
 
+    const uint64_t ukey = static_cast<uint64_t>(u) << 32;
+    const int64_t tmask = (1ll << a.track_shift) - 1;
     if (j < vend && S > 0.0 && wu > 0.0) {
       const double y0 = pbar_of(wu, w[j], S);
       int64_t vB = j, vsat = j;
@@ -640,7 +670,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       // ---- heavy band [vsat, vB): lane 0 walks exact per-class geometric skips ----
       if (vsat < vB) {
         int64_t jj = vsat;
-        int k = seg_of(a.seg, jj);
+        int k = seg_of_s(s_start, K, jj);
         int64_t seg_hi = 0;
         double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
         while (jj < vB) {
@@ -666,7 +696,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
               jj = seg_hi;
             } else {
               v = jj + delta;
-              const double r2 = unit53(rng.next());
+              const double r2 = unit53(rng.next_plus());
               if (pb >= 1.0) {
                 const double q = pbar_of(wu, w[v], S);
                 acc = q >= 1.0 || r2 < q;
@@ -683,13 +713,17 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       // ---- hazard envelope [vB, vend), cooperative rounds ----
       // Node ids are < 2^32 here (n <= 2^32 - 1, checked by set_weights).
       if (vB < vend) {
-        int k = seg_of(a.seg, vB);
+        int k = seg_of_s(s_start, K, vB);
         const double ymax = pbar_of(wu, s_wf[k], S);
         if (ymax > 0.0) {
-          const double kappa = __ddiv_rn(-log1p(-ymax), ymax);
+          // kappa = -log(1-y)/y = sum_k y^k/(k+1) (y < (1+eps)/16: 16 terms
+          // leave < 1e-19); reciprocals by one rcp each
+          double kappa = 1.0 / 17.0;
+#pragma unroll
+          for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
           const double c_u = kappa * (wu / S);
-          const double inv_c = 1.0 / c_u;
-          const double inv_kappa = 1.0 / kappa;
+          const double inv_c = __drcp_rn(c_u);
+          const double inv_kappa = __drcp_rn(kappa);
           double T0 = s_em[k] + s_wf[k] * static_cast<double>(vB - s_start[k]);
           uint32_t prev_v = static_cast<uint32_t>(vB - 1);
           const uint32_t vend32 = static_cast<uint32_t>(vend);
@@ -703,15 +737,13 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
           uint32_t pv = 0;
           double pr2 = 0.0, pf = 0.0, pw = 0.0;
           for (;;) {
-            if (kDefer) {
-              const bool accp = pend && pr2 < pw * pf;
-              WARP_EMIT(accp, pv)
-              pend = false;
-            }
+            const bool accp = kDefer && pend && pr2 < pw * pf;
+            const uint32_t pvv = pv;
+            pend = false;
             // Exp(1) by inversion with the shared log table
             double E;
             {
-              const double x = __dmul_rn(static_cast<double>(rng.next() >> 11) + 0.5, 0x1.0p-53);
+              const double x = __dmul_rn(static_cast<double>(rng.next_plus() >> 11) + 0.5, 0x1.0p-53);
               const long long bx = __double_as_longlong(x);
               const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
               const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
@@ -727,7 +759,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
               E = -__fma_rn(e, 0x1.62e42fefa39efp-1, s_log.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
             }
             const double T = T0 + warp_incl_scan_f64(E) * inv_c;
-            const double r2 = unit53(rng.next());
+            const double r2 = unit53(rng.next_plus());
             int kl = k;
             while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
             const uint32_t s0 = static_cast<uint32_t>(s_start[kl]);
@@ -756,12 +788,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
                 acc = r2 < g * (w[v] * iwf);
               }
             }
-            WARP_EMIT(acc, v)
+            WARP_EMIT2(accp, pvv, acc, v)
             // carry the last lane's event into the next round
             if (!__all_sync(CLG_FULL, valid)) {
               if (kDefer) {
-                const bool accp = pend && pr2 < pw * pf;
-                WARP_EMIT(accp, pv)
+                const bool accl = pend && pr2 < pw * pf;
+                WARP_EMIT(accl, pv)
               }
               break;
             }
@@ -777,6 +809,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       }
     }
 #undef WARP_EMIT
+#undef WARP_EMIT2
     if (MODE == kWalkCount && lane == 0) a.counts[unit] = cnt;
     if (MODE == kWalkFold && lane == 0 && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
       atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
