@@ -121,7 +121,7 @@ struct clgen_dev_ctx {
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
   // counter stream: weight-class segment table (per weights) and the hub
   // split plan of the last source range
-  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, hub_units, split_pos, unit_counts;
+  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.03125);
@@ -409,6 +409,7 @@ int ensure_segments(clgen_dev_ctx* c) {
   CUDA_TRY(c->seg_mass.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_em.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_invwf.ensure((kmax + 1) * sizeof(double)));
+  CUDA_TRY(c->seg_bucket.ensure(clg::kBuckets * sizeof(unsigned short)));
   double eps = c->seg_eps;
   for (int attempt = 0; attempt < 12; ++attempt, eps *= 2.0) {
     clg::build_segments_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, eps, kmax, c->seg_start.as<int64_t>(),
@@ -425,7 +426,8 @@ int ensure_segments(clgen_dev_ctx* c) {
       sg.K = K;
       clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
       clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>());
-      c->launches += 2;
+      clg::segment_buckets_kernel<<<clg::kBuckets / 256, 256, 0, c->stream>>>(sg, c->seg_bucket.as<unsigned short>());
+      c->launches += 3;
       CUDA_TRY(cudaGetLastError());
       c->seg_valid = true;
       return CLGEN_OK;
@@ -436,7 +438,8 @@ int ensure_segments(clgen_dev_ctx* c) {
 
 clg::Segments segments(clgen_dev_ctx* c) {
   return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
-                       c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K};
+                       c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
+                       c->seg_bucket.as<unsigned short>()};
 }
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected
@@ -815,6 +818,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->seg_mass.release();
   c->seg_em.release();
   c->seg_invwf.release();
+  c->seg_bucket.release();
   c->hub_units.release();
   c->split_pos.release();
   c->unit_counts.release();

@@ -58,7 +58,10 @@ struct Segments {
   const double* em;      // K+1 envelope-mass prefix: em[k+1] = em[k] + wfirst[k] * len_k
   const double* invwf;   // 1 / wfirst[k] (0 for a zero class)
   int K;
+  const unsigned short* bucket;  // kBuckets entries: class holding envelope mass b * em[K] / kBuckets
 };
+
+constexpr int kBuckets = 4096;
 
 constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA
 constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
@@ -243,7 +246,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     s_log.inv_c[i] = logtab->inv_c[i];
     s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
+  __shared__ unsigned short s_bucket[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
+  const double inv_bucket = static_cast<double>(kBuckets) / s_em[K];
 
   const int lane = lane_id();
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
@@ -387,9 +393,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           if (!(T < s_em[K])) {
             finish = true;
           } else {
-            do {
-              ++k;
-            } while (!(T < s_em[k + 1]));
+            const double bt = T * inv_bucket;
+            const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+            k = kb > k + 1 ? kb : k + 1;
+            while (!(T < s_em[k + 1])) ++k;
             em_next = s_em[k + 1];
             const double z = c_u * s_wf[k], z2 = z * z;
             gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
@@ -547,7 +554,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     s_log.inv_c[i] = logtab->inv_c[i];
     s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
+  __shared__ unsigned short s_bucket[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
+  const double inv_bucket = static_cast<double>(kBuckets) / s_em[K];
 
   const int lane = lane_id();
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
@@ -617,11 +627,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       } else if (MODE == kWalkFold) {                                                                   \
         if (ACCA) {                                                                                     \
           checksum += mix64(ukey | static_cast<uint64_t>(VA));                                          \
-          if (a.degree && ((VA) & tmask) == 0) atomicAdd(&a.degree[(VA) >> a.track_shift], 1u);        \
+          if (a.degree && (static_cast<uint32_t>(VA) & tmask) == 0) atomicAdd(&a.degree[(VA) >> a.track_shift], 1u);        \
         }                                                                                               \
         if (ACCB) {                                                                                     \
           checksum += mix64(ukey | static_cast<uint64_t>(VB));                                          \
-          if (a.degree && ((VB) & tmask) == 0) atomicAdd(&a.degree[(VB) >> a.track_shift], 1u);        \
+          if (a.degree && (static_cast<uint32_t>(VB) & tmask) == 0) atomicAdd(&a.degree[(VB) >> a.track_shift], 1u);        \
         }                                                                                               \
         edges_total += (lane == 0) ? kk_ : 0;                                                           \
         if (a.ring) {                                                                                   \
@@ -653,7 +663,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
 #define WARP_EMIT(ACC, VV) WARP_EMIT2(ACC, VV, false, 0u)
 
     const uint64_t ukey = static_cast<uint64_t>(u) << 32;
-    const int64_t tmask = (1ll << a.track_shift) - 1;
+    const uint32_t tmask = (1u << a.track_shift) - 1u;
     if (j < vend && S > 0.0 && wu > 0.0) {
       const double y0 = pbar_of(wu, w[j], S);
       int64_t vB = j, vsat = j;
@@ -760,8 +770,15 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             }
             const double T = T0 + warp_incl_scan_f64(E) * inv_c;
             const double r2 = unit53(rng.next_plus());
+            // class of T: bucket index (a lower bound) then a short forward walk
             int kl = k;
-            while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
+            if (!(T < s_em[k + 1])) {
+              const double bt = T * inv_bucket;
+              const int bi = bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1;
+              const int kb = s_bucket[bi];
+              kl = kb > k ? kb : k;
+              while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
+            }
             const uint32_t s0 = static_cast<uint32_t>(s_start[kl]);
             const uint32_t s1 = static_cast<uint32_t>(s_start[kl + 1]);
             const double iwf = s_iwf[kl];
@@ -1008,6 +1025,20 @@ __global__ void segment_mass_kernel(const double* __restrict__ w, Segments seg, 
     for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
     seg_mass[k] = t;
   }
+}
+
+// bucket[b] = largest k with em[k] <= b * em[K] / kBuckets (a lower bound of
+// the class of any T in bucket b).
+__global__ void segment_buckets_kernel(Segments seg, unsigned short* bucket) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= kBuckets) return;
+  const double x = seg.em[seg.K] * (static_cast<double>(b) / kBuckets);
+  int lo = 0, hi = seg.K;  // em[lo] <= x < em[hi] (or hi = K)
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (seg.em[m] <= x) lo = m; else hi = m;
+  }
+  bucket[b] = static_cast<unsigned short>(lo);
 }
 
 // First index in [lo,hi) with w < lim (hi if none); w non-increasing.  One warp.
