@@ -179,6 +179,16 @@ int clgen_dev_plan_block_costs(clgen_dev_ctx* ctx, int G, int g, double sigma_st
 int clgen_dev_plan_block_boundaries(clgen_dev_ctx* ctx, int G, int g, double z_offset,
                                     double z_bar, int64_t* found);
 
+/*
+ * Persist edges in the reference's formats (edge_io.cpp:72-88): binary
+ * CLGEDGE1 (16-byte header, u64 count, u64 pairs) or text "u v" lines.
+ * `pairs` (host or device, uint32 (u,v) pairs, `count` of them) are widened /
+ * rendered on the device chunk by chunk and streamed to `path`.  Errors as
+ * the reference: "cannot open for writing: <path>", "write failed: <path>".
+ */
+int clgen_dev_write_edges(clgen_dev_ctx* ctx, const uint32_t* pairs, int64_t count, int binary,
+                          const char* path);
+
 /* Ids of the sources flagged by the last generation call (up to cap). */
 int clgen_dev_flagged_nodes(clgen_dev_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
 

@@ -267,6 +267,10 @@ class _Ref:
         L.ref_global_cum_costs.argtypes = [vp, C.c_int, _dp, _dp, _dp]
         L.ref_generate_count.argtypes = [vp, C.c_int, C.c_int, _u64, _i64p, _dp, _dp, _i64p]
         L.ref_parallel_ranges_count.argtypes = [vp, C.c_double, _i64p, C.c_int, _u64, _i64p, _dp]
+        L.ref_write_edges.argtypes = [_u32p, _i64, C.c_int, C.c_char_p]
+        L.ref_read_edges.argtypes = [C.c_char_p, _u32p, _i64, _i64p]
+        L.ref_fidelity.argtypes = [vp, _u32p, _i64, C.c_double, _dp, C.POINTER(C.c_int), _dp, _i64p,
+                                   _dp, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]
 
     def _check(self, rc: int) -> None:
         if rc != 0:
@@ -390,6 +394,42 @@ class _Ref:
                                                 C.byref(gen_ms), C.byref(wall), _ptr(b, _i64p)))
         return {"edges": tot.value, "gen_wall_ms": gen_ms.value, "wall_ms": wall.value,
                 "boundaries": b}
+
+    def write_edges(self, pairs, path: str, binary: bool = True) -> None:
+        p = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)
+        self._check(self.lib.ref_write_edges(_ptr(p, _u32p), p.shape[0], int(binary),
+                                             path.encode()))
+
+    def read_edges(self, path: str) -> np.ndarray:
+        cnt = _i64()
+        self._check(self.lib.ref_read_edges(path.encode(), None, 0, C.byref(cnt)))
+        out = np.empty((max(cnt.value, 1), 2), np.uint32)
+        self._check(self.lib.ref_read_edges(path.encode(), _ptr(out, _u32p), cnt.value,
+                                            C.byref(cnt)))
+        return out[: cnt.value]
+
+    def fidelity(self, ws: RefWS, pairs, flag_mass: float = 100.0) -> dict:
+        """degree_histogram + compare_distributions (analysis.cpp:18-85)."""
+        p = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)
+        cap = 128
+        sc = np.zeros(5)
+        k = np.zeros(cap, np.int32)
+        ex = np.zeros(cap)
+        gen = np.zeros(cap, np.int64)
+        rel = np.zeros(cap)
+        fl = np.zeros(cap, np.int32)
+        nb = C.c_int()
+        ip = C.POINTER(C.c_int)
+        self._check(self.lib.ref_fidelity(ws.h, _ptr(p, _u32p), p.shape[0], flag_mass,
+                                          _ptr(sc, _dp), k.ctypes.data_as(ip), _ptr(ex, _dp),
+                                          _ptr(gen, _i64p), _ptr(rel, _dp), fl.ctypes.data_as(ip),
+                                          cap, C.byref(nb)))
+        m = min(nb.value, cap)
+        return {"mean_expected": sc[0], "mean_generated": sc[1], "mean_rel_error": sc[2],
+                "max_flagged_rel_error": sc[3], "zero_degree": int(sc[4]),
+                "bins": [{"k": int(k[i]), "expected_count": float(ex[i]),
+                          "generated_count": int(gen[i]), "rel_error": float(rel[i]),
+                          "flagged": bool(fl[i])} for i in range(m)]}
 
     def parallel_ranges_count(self, ws: RefWS, S, ranges, seed):
         r = np.ascontiguousarray(ranges, np.int64).reshape(-1)

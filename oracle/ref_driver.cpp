@@ -30,6 +30,8 @@
 #include <vector>
 
 #include "clgen/cost.hpp"
+#include "clgen/analysis.hpp"
+#include "clgen/edge_io.hpp"
 #include "clgen/edge_skip.hpp"
 #include "clgen/partition.hpp"
 #include "clgen/rng.hpp"
@@ -309,6 +311,59 @@ int ref_parallel_ranges_count(void* h, double S, const std::int64_t* ranges, int
     std::int64_t s = 0;
     for (auto c : counts) s += c;
     *total = s;
+  });
+}
+
+// edge_io.cpp:72-88 write_edges on uint32 pairs (widened to Edge).
+int ref_write_edges(const std::uint32_t* pairs, std::int64_t count, int binary, const char* path) {
+  return guard([&] {
+    std::vector<Edge> edges(static_cast<std::size_t>(count));
+    for (std::int64_t i = 0; i < count; ++i) edges[i] = Edge{pairs[2 * i], pairs[2 * i + 1]};
+    write_edges(edges, binary ? EdgeFormat::binary : EdgeFormat::text, path);
+  });
+}
+
+// edge_io.cpp:90-123 read_edges into uint32 pairs (cap entries); *count = records.
+int ref_read_edges(const char* path, std::uint32_t* pairs, std::int64_t cap, std::int64_t* count) {
+  return guard([&] {
+    const auto edges = read_edges(path);
+    *count = static_cast<std::int64_t>(edges.size());
+    for (std::int64_t i = 0; i < *count && i < cap; ++i) {
+      pairs[2 * i] = static_cast<std::uint32_t>(edges[i].u);
+      pairs[2 * i + 1] = static_cast<std::uint32_t>(edges[i].v);
+    }
+  });
+}
+
+// analysis.cpp:18-85: degree_histogram + compare_distributions on an edge
+// list.  Outputs: scalars[0..4] = mean_expected, mean_generated,
+// mean_rel_error, max_flagged_rel_error, zero_degree; per bin (up to cap):
+// k, expected_count, generated_count, rel_error, flagged.
+int ref_fidelity(void* h, const std::uint32_t* pairs, std::int64_t count, double flag_mass,
+                 double* scalars, int* bin_k, double* bin_expected, std::int64_t* bin_generated,
+                 double* bin_rel, int* bin_flagged, int cap, int* nbins) {
+  return guard([&] {
+    const auto& ws = *static_cast<WeightSequence*>(h);
+    std::vector<Edge> edges(static_cast<std::size_t>(count));
+    for (std::int64_t i = 0; i < count; ++i) edges[i] = Edge{pairs[2 * i], pairs[2 * i + 1]};
+    const auto hist = degree_histogram(edges, ws.size());
+    const auto rep = compare_distributions(ws, hist, flag_mass);
+    scalars[0] = rep.mean_expected;
+    scalars[1] = rep.mean_generated;
+    scalars[2] = rep.mean_rel_error;
+    scalars[3] = rep.max_flagged_rel_error;
+    scalars[4] = static_cast<double>(hist.zero_degree);
+    int i = 0;
+    for (const auto& b : rep.bins) {
+      if (i >= cap) break;
+      bin_k[i] = b.k;
+      bin_expected[i] = b.expected_count;
+      bin_generated[i] = b.generated_count;
+      bin_rel[i] = b.rel_error;
+      bin_flagged[i] = b.flagged ? 1 : 0;
+      ++i;
+    }
+    *nbins = static_cast<int>(rep.bins.size());
   });
 }
 

@@ -67,6 +67,7 @@ def _declare(L):
     L.clgen_dev_stream_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, C.c_int, _vp,
                                          C.c_int, _vp, _i64, _i64p, _u64p, _i64p]
     L.clgen_dev_flagged_nodes.argtypes = [_vp, _i64p, _i64, _i64p]
+    L.clgen_dev_write_edges.argtypes = [_vp, _vp, _i64, C.c_int, C.c_char_p]
     L.clgen_dev_generate_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, _vp, _i64,
                                            _i64p, _i64p]
     L.clgen_dev_set_counter_params.argtypes = [_vp, C.c_double, C.c_double]
@@ -96,7 +97,7 @@ EXPORTS = (
     "clgen_dev_plan_block_costs", "clgen_dev_plan_block_boundaries", "clgen_dev_generate_range",
     "clgen_dev_set_counter_params", "clgen_dev_counter_plan_info", "clgen_dev_set_fast_math",
     "clgen_dev_counter_heavy_units", "clgen_dev_set_warp_profile", "clgen_dev_warp_profile",
-    "clgen_dev_warp_profile_launches",
+    "clgen_dev_warp_profile_launches", "clgen_dev_write_edges",
 )
 
 

@@ -385,3 +385,96 @@ def generate_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
     check(L.clgen_dev_generate_range(ws.device.handle, S, lo, hi, seed & 0xFFFFFFFFFFFFFFFF, sm,
                                      _addr(out), int(out.shape[0]), C.byref(cnt), C.byref(nfl)))
     return out[: cnt.value]
+
+
+# ---- partitions other than UCP (partition.cpp:47-67) ----------------------
+@dataclass
+class PartitionPlan:
+    """partition.hpp:20-31 (boundaries for naive/ucp; strided for rrp)."""
+    scheme: str
+    procs: int
+    n: int
+    boundaries: np.ndarray | None = None
+
+    def partition_size(self, i: int) -> int:
+        if i < 0 or i >= self.procs:
+            raise error("partition_size: bad partition index")
+        if self.scheme == "rrp":
+            return (self.n - 1 - i) // self.procs + 1 if self.n > i else 0
+        return int(self.boundaries[i + 1] - self.boundaries[i])
+
+    def partition_nodes(self, i: int) -> np.ndarray:
+        """Ascending source nodes owned by partition i (partition.cpp:36-45)."""
+        if self.scheme == "rrp":
+            return np.arange(i, self.n, self.procs, dtype=np.int64)
+        return np.arange(self.boundaries[i], self.boundaries[i + 1], dtype=np.int64)
+
+
+def plan_naive(n: int, P: int) -> PartitionPlan:
+    """partition.cpp:47-57 (ceil-first blocks, cost.cpp:15-22)."""
+    if P < 1:
+        raise error("plan_naive: P must be >= 1")
+    from .plan import block_bounds
+    b = np.array([0] + [block_bounds(n, P, i)[1] for i in range(P)], np.int64)
+    return PartitionPlan("naive", P, n, b)
+
+
+def plan_rrp(n: int, P: int) -> PartitionPlan:
+    """partition.cpp:59-67 (u mod P)."""
+    if P < 1:
+        raise error("plan_rrp: P must be >= 1")
+    return PartitionPlan("rrp", P, n, None)
+
+
+def plan(ws: WeightSequence, scheme: str, P: int) -> PartitionPlan:
+    if scheme == "ucp":
+        return PartitionPlan("ucp", P, ws.size(), plan_ucp(ws, P))
+    if scheme == "naive":
+        return plan_naive(ws.size(), P)
+    if scheme == "rrp":
+        return plan_rrp(ws.size(), P)
+    raise error("unknown scheme: " + scheme)
+
+
+def generate_partition(ws: WeightSequence, p: PartitionPlan, i: int, seed: int):
+    """Partition i's edges, as generate_on_rank walks them (runtime.cpp:76-82)."""
+    if p.scheme == "rrp":
+        return create_edges(ws, ws.sum_S, p.partition_nodes(i), seed)
+    return create_edges_range(ws, ws.sum_S, int(p.boundaries[i]), int(p.boundaries[i + 1]), seed)
+
+
+# ---- edge files (edge_io.cpp) ---------------------------------------------
+def write_edges(edges, path: str, fmt: str = "binary", device: Device | None = None) -> None:
+    """edge_io.cpp:72-88; `edges` uint32[m,2] host array or device tensor."""
+    if fmt not in ("binary", "bin", "text"):
+        raise error("unknown edge format: " + fmt)
+    dev = device or default_device(0)
+    m = int(edges.shape[0])
+    check(_lib.lib().clgen_dev_write_edges(dev.handle, _addr(edges) if m else None, m,
+                                           int(fmt != "text"), path.encode()))
+
+
+def read_edges(path: str) -> np.ndarray:
+    """edge_io.cpp:90-123 (binary sniffed by magic, else text) -> uint32[m,2]."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:8] == b"CLGEDGE1":
+        if len(data) < 24:
+            raise error(f"{path}: truncated edge header")
+        ver = int.from_bytes(data[8:12], "little")
+        if ver != 1:
+            raise error(f"{path}: unsupported edge file version {ver}")
+        cnt = int.from_bytes(data[16:24], "little")
+        body = np.frombuffer(data, dtype="<u8", offset=24)
+        if body.size < 2 * cnt:
+            raise error(f"{path}: truncated at record {body.size // 2} of {cnt}")
+        return body[: 2 * cnt].reshape(-1, 2).astype(np.uint32)
+    rows = []
+    for lineno, line in enumerate(data.decode().splitlines(), 1):
+        if not line or line[0] == "#":
+            continue
+        parts = line.split()
+        if len(parts) < 2:
+            raise error(f"{path}: malformed edge at line {lineno}")
+        rows.append((int(parts[0]), int(parts[1])))
+    return np.array(rows, np.uint32).reshape(-1, 2)

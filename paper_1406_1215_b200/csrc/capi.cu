@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "exact_fold.cuh"
 #include "plan.cuh"
+#include "edge_io.cuh"
 #include "sampler_ctr.cuh"
 #include "sampler_ref.cuh"
 #include "scan.cuh"
@@ -136,6 +137,8 @@ struct clgen_dev_ctx {
   DevBuf prof;
   int prof_warps = 0;  // slots used by the last sampler launch(es)
   std::vector<int> prof_launch;  // first slot of each of those launches
+  void* host_stage = nullptr;    // pinned staging for edge files
+  size_t host_stage_bytes = 0;
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
@@ -801,6 +804,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->flagged) cudaFree(c->flagged);
   if (c->logtab) cudaFree(c->logtab);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->zig) cudaFree(c->zig);
   c->counts.release();
   c->offsets.release();
@@ -1215,6 +1219,77 @@ int clgen_dev_counter_plan_info(clgen_dev_ctx* c, int* classes, int64_t* hubs, i
   if (classes) *classes = c->seg_valid ? c->seg_K : 0;
   if (hubs) *hubs = c->ctr_H;
   if (units) *units = c->ctr_units;
+  return CLGEN_OK;
+}
+
+int clgen_dev_write_edges(clgen_dev_ctx* c, const uint32_t* pairs, int64_t count, int binary,
+                          const char* path) {
+  if (!c || !path || count < 0 || (count > 0 && !pairs)) return fail(CLGEN_EINVAL, "write_edges: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(CLGEN_EINVAL, "cannot open for writing: %s", path);
+  const bool dev_in = is_device_ptr(pairs);
+  constexpr int64_t kChunk = int64_t(1) << 23;  // edges per chunk
+  const int64_t chunk = count < kChunk ? count : kChunk;
+  auto done = [&](int code) {
+    std::fclose(f);
+    return code;
+  };
+  bool ok = true;
+  if (binary) {  // edge_io.cpp:80-86
+    unsigned char head[24] = {'C', 'L', 'G', 'E', 'D', 'G', 'E', '1', 1, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 8; ++i) head[16 + i] = static_cast<unsigned char>((static_cast<uint64_t>(count) >> (8 * i)) & 0xff);
+    ok = std::fwrite(head, 1, sizeof head, f) == sizeof head;
+  }
+  if (count > 0 && ok) {
+    const size_t out_bytes = binary ? static_cast<size_t>(chunk) * 16 : static_cast<size_t>(chunk) * 22;
+    if (c->pairs.ensure(chunk * sizeof(uint2)) != cudaSuccess || c->sources.ensure(out_bytes) != cudaSuccess ||
+        c->counts.ensure(chunk * sizeof(int32_t)) != cudaSuccess ||
+        c->offsets.ensure((chunk + 1) * sizeof(int64_t)) != cudaSuccess)
+      return done(fail(CLGEN_ENOMEM, "write_edges: cannot allocate staging buffers"));
+    if (c->host_stage_bytes < out_bytes) {
+      if (c->host_stage) cudaFreeHost(c->host_stage);
+      c->host_stage = nullptr;
+      c->host_stage_bytes = 0;
+      if (cudaMallocHost(&c->host_stage, out_bytes) != cudaSuccess)
+        return done(fail(CLGEN_ENOMEM, "write_edges: cannot allocate pinned staging"));
+      c->host_stage_bytes = out_bytes;
+    }
+    for (int64_t base = 0; base < count && ok; base += chunk) {
+      const int64_t m = count - base < chunk ? count - base : chunk;
+      const uint2* src = reinterpret_cast<const uint2*>(pairs) + base;
+      if (!dev_in) {
+        if (cudaMemcpyAsync(c->pairs.p, src, m * sizeof(uint2), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+          return done(fail(CLGEN_ECUDA, "write_edges: H2D copy failed"));
+        src = c->pairs.as<uint2>();
+      }
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, c->num_sms * 16));
+      size_t bytes = 0;
+      if (binary) {
+        clg::widen_pairs_kernel<<<grid, 256, 0, c->stream>>>(src, m, c->sources.as<unsigned long long>());
+        ++c->launches;
+        bytes = static_cast<size_t>(m) * 16;
+      } else {
+        int32_t* len = c->counts.as<int32_t>();
+        int64_t* off = c->offsets.as<int64_t>();
+        clg::text_len_kernel<<<grid, 256, 0, c->stream>>>(src, m, len);
+        ++c->launches;
+        if ((rc = launch_scan(c, len, off, m))) return done(rc);
+        if ((rc = fetch_scalars(c))) return done(rc);
+        bytes = static_cast<size_t>(c->sc_host->total);
+        clg::text_render_kernel<<<grid, 256, 0, c->stream>>>(src, m, off, c->sources.as<char>());
+        ++c->launches;
+      }
+      if (cudaGetLastError() != cudaSuccess ||
+          cudaMemcpyAsync(c->host_stage, c->sources.p, bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+          cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return done(fail(CLGEN_ECUDA, "write_edges: device staging failed"));
+      ok = std::fwrite(c->host_stage, 1, bytes, f) == bytes;
+    }
+  }
+  if (std::fclose(f) != 0) ok = false;
+  if (!ok) return fail(CLGEN_EINVAL, "write failed: %s", path);
   return CLGEN_OK;
 }
 
