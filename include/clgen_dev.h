@@ -189,6 +189,25 @@ int clgen_dev_plan_block_boundaries(clgen_dev_ctx* ctx, int G, int g, double z_o
 int clgen_dev_write_edges(clgen_dev_ctx* ctx, const uint32_t* pairs, int64_t count, int binary,
                           const char* path);
 
+/*
+ * Degree fidelity, the device analogue of degree_histogram +
+ * compare_distributions (analysis.cpp:18-85): `degree` (host or device,
+ * uint32, the undirected degree of every node, e.g. clgen_dev_stream_range
+ * with track_shift 0 or clgen_dev_edge_degrees) against the expected degree
+ * max(w - w^2/S, 0).  scalars[5] = mean_expected (bit-identical: the
+ * reference's sequential fold), mean_generated, mean_rel_error,
+ * max_flagged_rel_error, zero_degree.  Bins ascending by k = floor(log2 x):
+ * up to `cap` of (k, expected_count, generated_count, rel_error, flagged);
+ * *nbins = total bins.
+ */
+int clgen_dev_fidelity(clgen_dev_ctx* ctx, const uint32_t* degree, int64_t total_edges,
+                       double flag_mass, double* scalars, int* bin_k, double* bin_expected,
+                       int64_t* bin_generated, double* bin_rel, int* bin_flagged, int cap,
+                       int* nbins);
+/* Undirected degrees of a materialised edge list (uint32 pairs, host or
+ * device) into degree[n] (host or device). */
+int clgen_dev_edge_degrees(clgen_dev_ctx* ctx, const uint32_t* pairs, int64_t m, uint32_t* degree);
+
 /* Ids of the sources flagged by the last generation call (up to cap). */
 int clgen_dev_flagged_nodes(clgen_dev_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
 

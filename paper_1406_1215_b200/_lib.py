@@ -68,6 +68,10 @@ def _declare(L):
                                          C.c_int, _vp, _i64, _i64p, _u64p, _i64p]
     L.clgen_dev_flagged_nodes.argtypes = [_vp, _i64p, _i64, _i64p]
     L.clgen_dev_write_edges.argtypes = [_vp, _vp, _i64, C.c_int, C.c_char_p]
+    _ip = C.POINTER(C.c_int)
+    L.clgen_dev_fidelity.argtypes = [_vp, _vp, _i64, C.c_double, _dp, _ip, _dp, _i64p, _dp, _ip,
+                                     C.c_int, _ip]
+    L.clgen_dev_edge_degrees.argtypes = [_vp, _vp, _i64, _vp]
     L.clgen_dev_generate_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, _vp, _i64,
                                            _i64p, _i64p]
     L.clgen_dev_set_counter_params.argtypes = [_vp, C.c_double, C.c_double]
@@ -98,6 +102,7 @@ EXPORTS = (
     "clgen_dev_set_counter_params", "clgen_dev_counter_plan_info", "clgen_dev_set_fast_math",
     "clgen_dev_counter_heavy_units", "clgen_dev_set_warp_profile", "clgen_dev_warp_profile",
     "clgen_dev_warp_profile_launches", "clgen_dev_write_edges",
+    "clgen_dev_fidelity", "clgen_dev_edge_degrees",
 )
 
 

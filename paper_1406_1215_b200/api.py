@@ -478,3 +478,41 @@ def read_edges(path: str) -> np.ndarray:
             raise error(f"{path}: malformed edge at line {lineno}")
         rows.append((int(parts[0]), int(parts[1])))
     return np.array(rows, np.uint32).reshape(-1, 2)
+
+
+# ---- degree fidelity (analysis.cpp:18-85) ----------------------------------
+def edge_degrees(ws: WeightSequence, edges) -> np.ndarray:
+    """Undirected degrees (uint32[n]) of a materialised edge list."""
+    out = np.zeros(max(ws.size(), 1), np.uint32)
+    m = int(edges.shape[0])
+    check(_lib.lib().clgen_dev_edge_degrees(ws.device.handle, _addr(edges) if m else None, m,
+                                            out.ctypes.data))
+    return out[: ws.size()]
+
+
+def fidelity(ws: WeightSequence, degree, total_edges: int, flag_mass: float = 100.0) -> dict:
+    """compare_distributions(ws, degree_histogram(edges)) on the device."""
+    cap = 256
+    sc = np.zeros(5)
+    k = np.zeros(cap, np.int32)
+    ex = np.zeros(cap)
+    gen = np.zeros(cap, np.int64)
+    rel = np.zeros(cap)
+    fl = np.zeros(cap, np.int32)
+    nb = C.c_int()
+    if isinstance(degree, np.ndarray):
+        degree = np.ascontiguousarray(degree, np.uint32)
+    ip = C.POINTER(C.c_int)
+    check(_lib.lib().clgen_dev_fidelity(ws.device.handle, _addr(degree), int(total_edges),
+                                        float(flag_mass), sc.ctypes.data_as(C.POINTER(C.c_double)),
+                                        k.ctypes.data_as(ip),
+                                        ex.ctypes.data_as(C.POINTER(C.c_double)),
+                                        gen.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        rel.ctypes.data_as(C.POINTER(C.c_double)),
+                                        fl.ctypes.data_as(ip), cap, C.byref(nb)))
+    m = min(nb.value, cap)
+    return {"mean_expected": sc[0], "mean_generated": sc[1], "mean_rel_error": sc[2],
+            "max_flagged_rel_error": sc[3], "zero_degree": int(sc[4]),
+            "bins": [{"k": int(k[i]), "expected_count": float(ex[i]),
+                      "generated_count": int(gen[i]), "rel_error": float(rel[i]),
+                      "flagged": bool(fl[i])} for i in range(m)]}

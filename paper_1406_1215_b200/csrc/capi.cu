@@ -21,6 +21,7 @@
 #include "exact_fold.cuh"
 #include "plan.cuh"
 #include "edge_io.cuh"
+#include "fidelity.cuh"
 #include "sampler_ctr.cuh"
 #include "sampler_ref.cuh"
 #include "scan.cuh"
@@ -1290,6 +1291,98 @@ int clgen_dev_write_edges(clgen_dev_ctx* c, const uint32_t* pairs, int64_t count
   }
   if (std::fclose(f) != 0) ok = false;
   if (!ok) return fail(CLGEN_EINVAL, "write failed: %s", path);
+  return CLGEN_OK;
+}
+
+int clgen_dev_edge_degrees(clgen_dev_ctx* c, const uint32_t* pairs, int64_t m, uint32_t* degree) {
+  if (!c || m < 0 || (m > 0 && !pairs) || !degree) return fail(CLGEN_EINVAL, "edge_degrees: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  const bool dev_deg = is_device_ptr(degree);
+  CUDA_TRY(c->degree.ensure((n > 0 ? n : 1) * sizeof(uint32_t)));
+  uint32_t* d = dev_deg ? degree : c->degree.as<uint32_t>();
+  if (n > 0) CUDA_TRY(cudaMemsetAsync(d, 0, n * sizeof(uint32_t), c->stream));
+  const uint2* e = reinterpret_cast<const uint2*>(pairs);
+  if (m > 0 && !is_device_ptr(pairs)) {
+    CUDA_TRY(c->pairs.ensure(m * sizeof(uint2)));
+    CUDA_TRY(cudaMemcpyAsync(c->pairs.p, pairs, m * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
+    e = c->pairs.as<uint2>();
+  }
+  if (m > 0) {
+    clg::edge_degree_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(e, m, d);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (!dev_deg && n > 0) CUDA_TRY(cudaMemcpyAsync(degree, d, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
+int clgen_dev_fidelity(clgen_dev_ctx* c, const uint32_t* degree, int64_t total_edges, double flag_mass,
+                       double* scalars, int* bin_k, double* bin_expected, int64_t* bin_generated,
+                       double* bin_rel, int* bin_flagged, int cap, int* nbins) {
+  if (!c || !degree || !scalars || !nbins) return fail(CLGEN_EINVAL, "fidelity: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  double S;
+  if ((rc = blocked_sum_impl(c, c->w, n, &S))) return rc;
+  // histograms: [0, kFidBins) expected, [kFidBins, 2 kFidBins + 1) generated (+ zeros)
+  const size_t hbytes = (2 * clg::kFidBins + 1) * sizeof(unsigned long long);
+  CUDA_TRY(c->probe.ensure(hbytes));
+  unsigned long long* h = c->probe.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(h, 0, hbytes, c->stream));
+  const uint32_t* deg = degree;
+  if (n > 0 && !is_device_ptr(degree)) {
+    CUDA_TRY(c->degree.ensure(n * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpyAsync(c->degree.p, degree, n * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    deg = c->degree.as<uint32_t>();
+  }
+  double expected_sum = 0.0;
+  if (n > 0) {
+    CUDA_TRY(c->cum.ensure(n * sizeof(double)));
+    c->plan_G = 0;  // cum now holds expected degrees
+    double* d = c->cum.as<double>();
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, c->num_sms * 8));
+    clg::fid_expected_kernel<<<grid, 256, 0, c->stream>>>(c->w, n, S, d, h);
+    clg::fid_generated_kernel<<<grid, 256, 0, c->stream>>>(deg, n, h + clg::kFidBins);
+    c->launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    // analysis.cpp:53-58: expected_sum folded left to right over u
+    if ((rc = run_fold(c, d, n, 0.0, clg::kFoldNone, nullptr, nullptr, 0.0, &expected_sum))) return rc;
+  }
+  std::vector<unsigned long long> hv(2 * clg::kFidBins + 1);
+  CUDA_TRY(cudaMemcpy(hv.data(), h, hbytes, cudaMemcpyDeviceToHost));
+  const double dn = static_cast<double>(n);
+  const double mean_expected = n ? expected_sum / dn : 0.0;
+  const double mean_generated = n ? 2.0 * static_cast<double>(total_edges) / dn : 0.0;
+  scalars[0] = mean_expected;
+  scalars[1] = mean_generated;
+  scalars[2] = mean_expected > 0.0 ? std::fabs(mean_generated - mean_expected) / mean_expected
+                                   : std::fabs(mean_generated);
+  double max_flagged = 0.0;
+  int nb = 0;
+  for (int i = 0; i < clg::kFidBins; ++i) {
+    const unsigned long long ec = hv[i], gc = hv[clg::kFidBins + i];
+    if (!ec && !gc) continue;
+    const double exp_count = static_cast<double>(ec);
+    const bool flagged = exp_count >= flag_mass;
+    const double rel = exp_count > 0.0 ? std::fabs(static_cast<double>(gc) - exp_count) / exp_count
+                                       : (gc == 0 ? 0.0 : 1.0);
+    if (flagged && rel > max_flagged) max_flagged = rel;
+    if (nb < cap) {
+      if (bin_k) bin_k[nb] = i - clg::kFidBinOff;
+      if (bin_expected) bin_expected[nb] = exp_count;
+      if (bin_generated) bin_generated[nb] = static_cast<int64_t>(gc);
+      if (bin_rel) bin_rel[nb] = rel;
+      if (bin_flagged) bin_flagged[nb] = flagged ? 1 : 0;
+    }
+    ++nb;
+  }
+  scalars[3] = max_flagged;
+  scalars[4] = static_cast<double>(hv[2 * clg::kFidBins]);
+  *nbins = nb;
   return CLGEN_OK;
 }
 

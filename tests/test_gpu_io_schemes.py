@@ -73,3 +73,26 @@ def test_plan_shapes(api):
     assert r.partition_size(0) == 3 and r.partition_size(1) == 2
     with pytest.raises(api.error):
         api.plan_naive(4, 0)
+
+
+def test_fidelity_matches_reference(api, ref):
+    """(f1): device degree-fidelity report == analysis.cpp's, bit for bit."""
+    for (n, g, lo, hi, s_w, s_g) in [(100_000, 2.5, 50.0, 800.0, 0xF1DF, 0xF1E0),  # acceptance.cpp:276
+                                     (200_000, 2.1, 2.0, 1e4, 5, 6)]:
+        rws = ref.synth_powerlaw(n, g, lo, hi, s_w)
+        ws = api.make_weight_sequence(rws.weights)
+        edges = api.serial_cl(ws, s_g)
+        ours_deg = api.edge_degrees(ws, edges)
+        streamed = api.stream_range(ws, ws.sum_S, 0, n, s_g, track_shift=0)
+        np.testing.assert_array_equal(streamed.degree, ours_deg)
+        got = api.fidelity(ws, ours_deg, len(edges), 100.0)
+        exp = ref.fidelity(rws, edges, 100.0)
+        for key in ("mean_expected", "mean_generated", "mean_rel_error", "max_flagged_rel_error",
+                    "zero_degree"):
+            assert got[key] == exp[key], key
+        assert got["bins"] == exp["bins"]
+    # constant weights (acceptance.cpp:260-266): mean degree within 2%
+    cws = api.make_weight_sequence(np.full(100_000, 50.0))
+    r = api.stream_range(cws, cws.sum_S, 0, 100_000, 0xF1DE, track_shift=0)
+    rep = api.fidelity(cws, r.degree, r.count)
+    assert rep["mean_rel_error"] <= 0.02
