@@ -143,6 +143,7 @@ struct clgen_dev_ctx {
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
+  int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 1.0));
   clg::LogTable* logtab = nullptr;  // device
   clg::ZigTable* zig = nullptr;     // device
   // instrumentation: kernels launched by this context, and the duration of
@@ -240,6 +241,7 @@ clg::RefWalkArgs walk_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   a.ring_head = &c->sc->ring_head;
   a.logtab = c->logtab;
   a.invS = 1.0 / S;  // host IEEE division: RN(1/S)
+  a.refill_min = c->refill_min;
   return a;
 }
 

@@ -45,6 +45,7 @@ struct RefWalkArgs {
   // fast math (bit-exact with guarded fallbacks, fastmath.cuh)
   const LogTable* logtab;
   double invS;                   // RN(1/S)
+  int refill_min;                // refill idle lanes only when at least this many are idle
 };
 
 // Skip length exactly as edge_skip.cpp:9-16 computes it, with CUDA's libm.
@@ -66,8 +67,15 @@ __device__ __forceinline__ int64_t skip_length_ref(double p, double r, bool& amb
 // Skip length with the fast guarded ratio; the exact reference expression
 // (and its glibc-vs-CUDA ambiguity flag) only inside a 2^-45 band around an
 // integer, where the fast ratio (error <= ~2^-48) cannot certify the floor.
-__device__ __forceinline__ int64_t skip_length_fast(double p, double r, bool& amb, const LogTable& T) {
-  const double ratio = log_fast(r, T) * __drcp_rn(log1m_fast(p, T));
+// ilp caches 1/log1p(-p) for the p it was computed for (lp_p): consecutive
+// candidates with equal weights (C2: always; discrete weights: often) reuse it.
+__device__ __forceinline__ int64_t skip_length_fast(double p, double r, bool& amb, const LogTable& T,
+                                                    double& lp_p, double& ilp) {
+  if (p != lp_p) {
+    ilp = __drcp_rn(log1m_fast(p, T));
+    lp_p = p;
+  }
+  const double ratio = log_fast(r, T) * ilp;
   const double fl = floor(ratio);
   const double tol = ratio * 0x1p-45;
   if (ratio < 1.0e18 && !((ratio - fl <= tol && fl >= 1.0) || (fl + 1.0) - ratio <= tol))
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   // lane state
   int64_t u = -1, slot = 0, j = 0, out_pos = 0;
   int32_t cnt = 0;
-  double p = 0.0, wu = 0.0;
+  double p = 0.0, wu = 0.0, lp_p = -1.0, ilp = 0.0;
   bool amb = false;
   Xoshiro rng;
   uint64_t checksum = 0;
@@ -111,7 +119,9 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   for (;;) {
     // ---------------------------------------------------------------- refill
     const unsigned need = __ballot_sync(CLG_FULL, u < 0);
-    if (need && !drained) {
+    // refill when enough lanes are idle (a lone refill would stall the long
+    // chains sharing the warp) or when the whole warp is idle
+    if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
       const int want = __popc(need);
       const int r = __popc(need & lanemask_lt());
       const bool me = (need >> lane) & 1u;
@@ -165,7 +175,8 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         finish = true;  // edge_skip.cpp:31 loop condition
       } else {
         int64_t delta = 0;
-        if (p < 1.0) delta = FAST ? skip_length_fast(p, rng.open01(), amb, s_tab) : skip_length_ref(p, rng.open01(), amb);
+        if (p < 1.0)
+          delta = FAST ? skip_length_fast(p, rng.open01(), amb, s_tab, lp_p, ilp) : skip_length_ref(p, rng.open01(), amb);
         if (delta >= n - j) {
           finish = true;  // edge_skip.cpp:34
         } else {
