@@ -143,7 +143,7 @@ struct clgen_dev_ctx {
   uint64_t seed_mix = 0;
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
-  int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 1.0));
+  int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
   clg::LogTable* logtab = nullptr;  // device
   clg::ZigTable* zig = nullptr;     // device
   // instrumentation: kernels launched by this context, and the duration of
