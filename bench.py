@@ -143,26 +143,34 @@ def cpu_sample_ranges(w: np.ndarray, target_edges: float, k: int):
     return ranges
 
 
-def cpu_baseline(w: np.ndarray, seed: int, seconds: float, kind: str = "reference"):
-    """Time the reference CPU generator (oracle/_ref: the unmodified reference
-    library) on a bounded sample of the workload, all host threads in
-    parallel (the acceptance.cpp:221-254 per-partition pattern)."""
-    import oracle
-    cores = os.cpu_count() or 1
-    R = oracle.ref()
-    ws = R.weight_sequence(w)
-    # calibrate: ~0.2 s single-range probe for the per-thread rate
-    probe = cpu_sample_ranges(w, 2e5, 1)
-    tot, ms = R.parallel_ranges_count(ws, ws.sum_S, probe, seed)
-    rate1 = max(tot / max(ms, 1e-3) * 1e3, 1e5)
-    per_thread_edges = rate1 * seconds
-    ranges = cpu_sample_ranges(w, per_thread_edges, cores)
-    tot, ms = R.parallel_ranges_count(ws, ws.sum_S, ranges, seed)
-    del ws
-    return {"value": tot / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{cores} source ranges spread over [0,n), ~{per_thread_edges:.3g} expected "
-                      f"edges each, create_edges_range in parallel std::threads; "
-                      f"{tot} edges in {ms / 1e3:.2f} s"}
+class CpuReference:
+    """The reference CPU generator (oracle/_ref: the unmodified reference
+    library) on a bounded sample of the workload: `cores` source ranges
+    spread evenly over [0, n), each with about `seconds` of expected work per
+    thread, timed with create_edges_range in parallel std::threads (the
+    acceptance.cpp:221-254 per-partition pattern), count-only sink."""
+
+    def __init__(self, w: np.ndarray, seconds: float):
+        import oracle
+        self.cores = os.cpu_count() or 1
+        self.R = oracle.ref()
+        self.ws = self.R.weight_sequence(w)
+        probe = cpu_sample_ranges(w, 2e5, 1)  # ~0.1 s single-range probe: per-thread rate
+        tot, ms = self.R.parallel_ranges_count(self.ws, self.ws.sum_S, probe, 1)
+        rate1 = max(tot / max(ms, 1e-3) * 1e3, 1e5)
+        self.per_thread_edges = rate1 * seconds
+        self.ranges = cpu_sample_ranges(w, self.per_thread_edges, self.cores)
+
+    def step(self, seed: int) -> dict:
+        tot, ms = self.R.parallel_ranges_count(self.ws, self.ws.sum_S, self.ranges, seed)
+        return {"value": tot / (ms / 1e3), "unit": UNIT, "cores": self.cores, "kind": "reference",
+                "sample": f"{self.cores} source ranges spread over [0,n), "
+                          f"~{self.per_thread_edges:.3g} expected edges each, create_edges_range "
+                          f"in parallel std::threads; {tot} edges in {ms / 1e3:.2f} s"}
+
+
+def cpu_baseline(w: np.ndarray, seed: int, seconds: float) -> dict:
+    return CpuReference(w, seconds).step(seed)
 
 
 def run_reference(args):
@@ -172,11 +180,12 @@ def run_reference(args):
     from paper_1406_1215_b200 import workloads
     w = workloads.make(args.config, args.n)
     seed = workloads.WORKLOADS[args.config].seed
-    vals = []
+    ref = CpuReference(w, args.cpu_seconds / 2)
+    vals, last = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(w, seed + i, args.cpu_seconds / 2)
+        last = ref.step(seed + i)
         if i >= args.warmup:
-            vals.append(r["value"])
+            vals.append(last["value"])
     v = float(np.median(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
@@ -184,7 +193,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {workloads.WORKLOADS[args.config].desc}",
                    "n": int(w.size)},
-        "cpu_baseline": {**r, "value": v},
+        "cpu_baseline": {**last, "value": v},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
