@@ -608,10 +608,9 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     const unsigned ba_ = __ballot_sync(CLG_FULL, ACCA);                                                 \
     const unsigned bb_ = __ballot_sync(CLG_FULL, ACCB);                                                 \
     if (ba_ | bb_) {                                                                                    \
-      const unsigned ka_ = __popc(ba_);                                                                 \
-      const unsigned kk_ = ka_ + __popc(bb_);                                                           \
-      const unsigned ra_ = __popc(ba_ & lt_mask);                                                       \
-      const unsigned rb_ = ka_ + __popc(bb_ & lt_mask);                                                 \
+      const unsigned kk_ = __popc(ba_) + __popc(bb_);                                                   \
+      const unsigned ra_ = __popc(ba_ & lt_mask) + __popc(bb_ & lt_mask);                               \
+      const unsigned rb_ = ra_ + ((ACCA) ? 1u : 0u);                                                    \
       if (MODE == kWalkWrite) {                                                                         \
         if (ACCA) {                                                                                     \
           const int64_t pos_ = out_pos + ra_;                                                           \
@@ -743,80 +742,113 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
           // count/fold modes resolve an uncertain accept one round later (its
           // w[v] load overlaps the next round); the ordered write pass cannot
           constexpr bool kDefer = MODE != kWalkWrite;
-          bool pend = false;
-          uint32_t pv = 0;
-          double pr2 = 0.0, pf = 0.0, pw = 0.0;
-          for (;;) {
-            const bool accp = kDefer && pend && pr2 < pw * pf;
-            const uint32_t pvv = pv;
-            pend = false;
-            // Exp(1) by inversion with the shared log table
-            double E;
-            {
-              const double x = __dmul_rn(static_cast<double>(rng.next_plus() >> 11) + 0.5, 0x1.0p-53);
-              const long long bx = __double_as_longlong(x);
-              const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
-              const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
-              const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-              const double t = __fma_rn(m, s_log.inv_c[ti], -1.0);
-              double sp = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
-              sp = __fma_rn(t, sp, 1.0 / 5.0);
-              sp = __fma_rn(t, sp, -1.0 / 4.0);
-              sp = __fma_rn(t, sp, 1.0 / 3.0);
-              sp = __fma_rn(t, sp, -0.5);
-              sp = __fma_rn(t, sp, 1.0);
-              const double e = static_cast<double>(ex);
-              E = -__fma_rn(e, 0x1.62e42fefa39efp-1, s_log.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
-            }
-            const double T = T0 + warp_incl_scan_f64(E) * inv_c;
-            const double r2 = unit53(rng.next_plus());
-            // class of T: bucket index (a lower bound) then a short forward walk
-            int kl = k;
-            if (!(T < s_em[k + 1])) {
+          bool penda = false, pendb = false;
+          uint32_t pva = 0, pvb = 0;
+          double pr2a = 0.0, pfa = 0.0, pwa = 0.0, pr2b = 0.0, pfb = 0.0, pwb = 0.0;
+          // Exp(1) by inversion with the shared log table
+          auto exp1 = [&]() -> double {
+            const double x = __dmul_rn(static_cast<double>(rng.next_plus() >> 11) + 0.5, 0x1.0p-53);
+            const long long bx = __double_as_longlong(x);
+            const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
+            const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
+            const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+            const double t = __fma_rn(m, s_log.inv_c[ti], -1.0);
+            double sp = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
+            sp = __fma_rn(t, sp, 1.0 / 5.0);
+            sp = __fma_rn(t, sp, -1.0 / 4.0);
+            sp = __fma_rn(t, sp, 1.0 / 3.0);
+            sp = __fma_rn(t, sp, -0.5);
+            sp = __fma_rn(t, sp, 1.0);
+            const double e = static_cast<double>(ex);
+            return -__fma_rn(e, 0x1.62e42fefa39efp-1, s_log.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
+          };
+          // class of T, at or after class kf: bucket index (a lower bound) then a forward walk
+          auto class_of = [&](double T, int kf) -> int {
+            int kl = kf;
+            if (!(T < s_em[kf + 1])) {
               const double bt = T * inv_bucket;
-              const int bi = bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1;
-              const int kb = s_bucket[bi];
-              kl = kb > k ? kb : k;
+              const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+              kl = kb > kf ? kb : kf;
               while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
             }
+            return kl;
+          };
+          auto position = [&](double T, int kl) -> uint32_t {
             const uint32_t s0 = static_cast<uint32_t>(s_start[kl]);
             const uint32_t s1 = static_cast<uint32_t>(s_start[kl + 1]);
-            const double iwf = s_iwf[kl];
-            uint32_t v = s0 + static_cast<uint32_t>(fmax(T - s_em[kl], 0.0) * iwf);
-            if (v > s1 - 1) v = s1 - 1;
-            const bool valid = T < em_end && v < vend32;
-            uint32_t vp = __shfl_up_sync(CLG_FULL, v, 1);
+            uint32_t v = s0 + static_cast<uint32_t>(fmax(T - s_em[kl], 0.0) * s_iwf[kl]);
+            return v > s1 - 1 ? s1 - 1 : v;
+          };
+          // lane l takes events 2l and 2l+1 of each 64-event round
+          for (;;) {
+            const bool accpa = kDefer && penda && pr2a < pwa * pfa;
+            const bool accpb = kDefer && pendb && pr2b < pwb * pfb;
+            const uint32_t pvva = pva, pvvb = pvb;
+            penda = pendb = false;
+            const double Ea = exp1();
+            const double Eb = exp1();
+            const double pair = Ea + Eb;
+            const double incl = warp_incl_scan_f64(pair);
+            const double Ta = T0 + (incl - Eb) * inv_c;
+            const double Tb = T0 + incl * inv_c;
+            const double r2a = unit53(rng.next_plus());
+            const double r2b = unit53(rng.next_plus());
+            const int kla = class_of(Ta, k);
+            const int klb = class_of(Tb, kla);
+            const uint32_t va = position(Ta, kla);
+            const uint32_t vb = position(Tb, klb);
+            const bool valida = Ta < em_end && va < vend32;
+            const bool validb = Tb < em_end && vb < vend32;
+            uint32_t vp = __shfl_up_sync(CLG_FULL, vb, 1);
             if (lane == 0) vp = prev_v;
-            const bool propose = valid && v > vp;
-            const int di = kl - kw;
-            double g = __shfl_sync(CLG_FULL, g_lane, di & 31);
-            if (di >= 32) g = bern_gk(inv_kappa, c_u * s_wf[kl]);
-            bool acc = false;
-            if (propose) {
-              if (r2 < s_sure[kl] * g) {
-                acc = true;
+            const bool propa = valida && va > vp;
+            const bool propb = validb && vb > va;
+            const int dia = kla - kw, dib = klb - kw;
+            double ga = __shfl_sync(CLG_FULL, g_lane, dia & 31);
+            double gb = __shfl_sync(CLG_FULL, g_lane, dib & 31);
+            if (dia >= 32) ga = bern_gk(inv_kappa, c_u * s_wf[kla]);
+            if (dib >= 32) gb = bern_gk(inv_kappa, c_u * s_wf[klb]);
+            bool acca = false, accb = false;
+            if (propa) {
+              if (r2a < s_sure[kla] * ga) {
+                acca = true;
               } else if (kDefer) {
-                pend = true;
-                pv = v;
-                pr2 = r2;
-                pf = g * iwf;
-                pw = w[v];  // consumed next round
+                penda = true;
+                pva = va;
+                pr2a = r2a;
+                pfa = ga * s_iwf[kla];
+                pwa = w[va];  // consumed next round
               } else {
-                acc = r2 < g * (w[v] * iwf);
+                acca = r2a < ga * (w[va] * s_iwf[kla]);
               }
             }
-            WARP_EMIT2(accp, pvv, acc, v)
-            // carry the last lane's event into the next round
-            if (!__all_sync(CLG_FULL, valid)) {
+            if (propb) {
+              if (r2b < s_sure[klb] * gb) {
+                accb = true;
+              } else if (kDefer) {
+                pendb = true;
+                pvb = vb;
+                pr2b = r2b;
+                pfb = gb * s_iwf[klb];
+                pwb = w[vb];
+              } else {
+                accb = r2b < gb * (w[vb] * s_iwf[klb]);
+              }
+            }
+            if (kDefer) WARP_EMIT2(accpa, pvva, accpb, pvvb)
+            WARP_EMIT2(acca, va, accb, vb)
+            // carry the last lane's second event into the next round
+            if (!__all_sync(CLG_FULL, validb)) {
               if (kDefer) {
-                const bool accl = pend && pr2 < pw * pf;
-                WARP_EMIT(accl, pv)
+                const bool la = penda && pr2a < pwa * pfa;
+                const bool lb = pendb && pr2b < pwb * pfb;
+                WARP_EMIT2(la, pva, lb, pvb)
               }
               break;
             }
-            T0 = __shfl_sync(CLG_FULL, T, 31);
-            k = __shfl_sync(CLG_FULL, kl, 31);
-            prev_v = __shfl_sync(CLG_FULL, v, 31);
+            T0 = __shfl_sync(CLG_FULL, Tb, 31);
+            k = __shfl_sync(CLG_FULL, klb, 31);
+            prev_v = __shfl_sync(CLG_FULL, vb, 31);
             if (k - kw >= 16) {
               kw = k;
               g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
