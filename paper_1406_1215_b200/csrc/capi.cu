@@ -592,8 +592,8 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
   if (c->ctr_heavy > 0) {
     static const int wminb = [] {
       const char* e = std::getenv("CLGEN_WARP_MINB");
-      const int v = e ? std::atoi(e) : 4;
-      return v >= 2 && v <= 4 ? v : 4;
+      const int v = e ? std::atoi(e) : 3;
+      return v >= 2 && v <= 4 ? v : 3;
     }();
     if (!c->ctr_warp_blocks[MODE]) {
       int per_sm = 0;
