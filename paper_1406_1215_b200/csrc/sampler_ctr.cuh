@@ -676,47 +676,53 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
         const bool acc = v < vsat;
         WARP_EMIT(acc, v)
       }
-      // ---- heavy band [vsat, vB): lane 0 walks exact per-class geometric skips ----
+      // ---- heavy band [vsat, vB): per class a Bernoulli(pbar_k) process,
+      // cooperatively: lane i draws a geometric gap, an integer warp prefix
+      // sum places 32 candidates; a gap past the class end restarts at the
+      // next class (memoryless) ----
       if (vsat < vB) {
         int64_t jj = vsat;
         int k = seg_of_s(s_start, K, jj);
-        int64_t seg_hi = 0;
-        double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
         while (jj < vB) {
-          bool acc = false;
-          int64_t v = 0;
-          if (lane == 0) {
-            if (jj >= seg_hi) {
-              while (s_start[k + 1] <= jj) ++k;
-              seg_hi = imin64(s_start[k + 1], vB);
-              wf = s_wf[k];
-              pb = fmin(pbar_of(wu, wf, S), 1.0);
-              sure = s_sure[k];
-              ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
-            }
-            int64_t delta = 0;
-            bool over = false;
-            if (pb < 1.0) {
-              const double ratio = log(rng.open01()) * ilp;
-              if (!(ratio < static_cast<double>(seg_hi - jj))) over = true;
-              else delta = static_cast<int64_t>(ratio);
-            }
-            if (over) {
-              jj = seg_hi;
-            } else {
-              v = jj + delta;
-              const double r2 = unit53(rng.next_plus());
-              if (pb >= 1.0) {
+          while (s_start[k + 1] <= jj) ++k;
+          const int64_t seg_hi = imin64(s_start[k + 1], vB);
+          const double wf = s_wf[k];
+          const double pb = fmin(pbar_of(wu, wf, S), 1.0);
+          if (pb >= 1.0) {
+            // envelope 1: every position is a candidate, accepted with q
+            for (int64_t p0 = jj; p0 < seg_hi; p0 += 32) {
+              const int64_t v = p0 + lane;
+              bool acc = false;
+              if (v < seg_hi) {
                 const double q = pbar_of(wu, w[v], S);
-                acc = q >= 1.0 || r2 < q;
-              } else {
+                acc = q >= 1.0 || unit53(rng.next_plus()) < q;
+              }
+              WARP_EMIT(acc, v)
+            }
+            jj = seg_hi;
+          } else {
+            const double imu = 1.0 / -log1p(-pb);  // geometric gap: floor(E / mu) + 1
+            const double sure = s_sure[k];
+            for (;;) {
+              const double x = unit53(rng.next_plus()) + 0x1.0p-54;  // (0,1)
+              const double ratio = -log(x) * imu;
+              const int64_t gap = ratio < 4.0e18 ? static_cast<int64_t>(ratio) + 1 : (int64_t(1) << 62);
+              const int64_t off = warp_inclusive_scan(gap);  // gaps >= 1: positions strictly increase
+              const int64_t v = jj + off - 1;
+              const bool valid = off <= seg_hi - jj;
+              bool acc = false;
+              if (valid) {
+                const double r2 = unit53(rng.next_plus());
                 acc = r2 < sure || r2 * wf < w[v];
               }
-              jj = v + 1;
+              WARP_EMIT(acc, v)
+              if (!__all_sync(CLG_FULL, valid)) break;
+              jj = __shfl_sync(CLG_FULL, v, 31) + 1;
+              if (jj >= seg_hi) break;
             }
+            jj = seg_hi;
           }
-          jj = __shfl_sync(CLG_FULL, jj, 0);
-          WARP_EMIT(acc, v)
+          ++k;
         }
       }
       // ---- hazard envelope [vB, vend), cooperative rounds ----
