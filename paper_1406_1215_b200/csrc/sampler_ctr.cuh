@@ -344,10 +344,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
             // kappa = -log(1-ymax)/ymax from the largest envelope used
             const double ymax = pbar_of(wu, s_wf[kb], S);
             if (ymax > 0.0) {
-              const double kappa = __ddiv_rn(-log1p(-ymax), ymax);
+              double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
+#pragma unroll
+              for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
               c_u = kappa * (wu / S);
-              inv_c = 1.0 / c_u;
-              inv_kappa = 1.0 / kappa;
+              inv_c = __drcp_rn(c_u);
+              inv_kappa = __drcp_rn(kappa);
               T = s_em[kb] + s_wf[kb] * static_cast<double>(vB - s_start[kb]);
               prev_v = vB - 1;
               k = kb;
