@@ -126,7 +126,7 @@ struct clgen_dev_ctx {
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   bool seg_valid = false;
-  double seg_eps = env_double("CLGEN_CTR_EPS", 0.03125);
+  double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
   double heavy_cand = env_double("CLGEN_CTR_HEAVY", 128.0);  // units with >= this many expected candidates run warp-cooperatively

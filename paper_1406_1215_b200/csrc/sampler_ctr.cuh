@@ -63,7 +63,7 @@ struct Segments {
 
 constexpr int kBuckets = 4096;
 
-constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA
+constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA (static smem < 48 KB)
 constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
 
 struct CtrWalkArgs {
