@@ -145,7 +145,6 @@ struct clgen_dev_ctx {
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
   clg::LogTable* logtab = nullptr;  // device
-  clg::ZigTable* zig = nullptr;     // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
   unsigned long long launches = 0;
@@ -543,10 +542,7 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   a.S = S;
   a.lo = lo;
   a.hi = hi;
-  const uint64_t key = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
-  a.key0 = static_cast<uint32_t>(key);
-  a.key1 = static_cast<uint32_t>(key >> 32);
-  c->seed_mix = key;
+  c->seed_mix = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
   a.seg = segments(c);
   a.H = c->ctr_H;
   a.hub_units = c->hub_units.as<int64_t>();
@@ -762,8 +758,7 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
       cudaMalloc(&c->flagged, kFlagCap * sizeof(int64_t)) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess ||
-      cudaMalloc(&c->zig, sizeof(clg::ZigTable)) != cudaSuccess) {
+      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess) {
     clgen_dev_destroy(c);
     return fail(CLGEN_ENOMEM, "clgen_dev_create: allocation failed");
   }
@@ -775,21 +770,7 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       t.inv_c[i] = static_cast<double>(1.0L / ci);
       t.nlog_inv[i] = static_cast<double>(-logl(static_cast<long double>(t.inv_c[i])));
     }
-    // exponential ziggurat layers (256): x[1] = r, x[i+1] = -log(v/x[i] + e^-x[i])
-    clg::ZigTable z;
-    const long double r = 7.69711747013104972L;
-    const long double v = (r + 1.0L) * expl(-r);
-    long double xi = r;
-    z.x[0] = static_cast<double>(v * expl(r));
-    z.x[1] = static_cast<double>(r);
-    for (int i = 1; i < clg::kZigLayers; ++i) {
-      xi = -logl(v / xi + expl(-xi));
-      z.x[i + 1] = static_cast<double>(xi);
-    }
-    z.x[clg::kZigLayers] = 0.0;
-    for (int i = 0; i <= clg::kZigLayers; ++i) z.f[i] = static_cast<double>(expl(-static_cast<long double>(z.x[i])));
-    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->zig, &z, sizeof z, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess) {
       clgen_dev_destroy(c);
       return fail(CLGEN_ECUDA, "clgen_dev_create: cannot upload log table");
     }
@@ -808,7 +789,6 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (c->flagged) cudaFree(c->flagged);
   if (c->logtab) cudaFree(c->logtab);
   if (c->host_stage) cudaFreeHost(c->host_stage);
-  if (c->zig) cudaFree(c->zig);
   c->counts.release();
   c->offsets.release();
   c->tiles.release();

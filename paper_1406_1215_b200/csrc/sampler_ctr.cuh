@@ -1,5 +1,6 @@
-// Counter-stream Chung–Lu sampler (the north star's counter-based RNG keyed by
-// (seed, u, draw index)).  Statistically exact, not stream-identical to the
+// Counter-stream Chung–Lu sampler (the north star's keyed RNG: every draw is a
+// function of (seed, u, split, lane, draw index)).  Statistically exact, not
+// stream-identical to the
 // reference: every pair (u, v>u) appears independently with probability
 // min(w_u w_v / S, 1), the law of edges_from_source (edge_skip.cpp:20-46).
 //
@@ -28,23 +29,6 @@
 
 namespace clg {
 
-// ---- Philox4x32-10 (Salmon et al., SC'11) --------------------------------
-struct P4 {
-  uint32_t x, y, z, w;
-};
-
-__device__ __forceinline__ P4 philox4x32_10(P4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = P4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return c;
-}
-
 // 53-bit uniform strictly inside (0,1): (x>>11 + 1/2) * 2^-53.
 __device__ __forceinline__ double u53(uint32_t hi, uint32_t lo) {
   const uint64_t x = (static_cast<uint64_t>(hi) << 32) | lo;
@@ -71,7 +55,6 @@ struct CtrWalkArgs {
   int64_t n;
   double S;
   int64_t lo, hi;          // source range [lo,hi)
-  uint32_t key0, key1;     // Philox key from the seed
   Segments seg;
   // hub splitting: sources [lo, lo+H) are split; unit prefix over them
   int64_t H;
@@ -128,15 +111,6 @@ __device__ __forceinline__ int64_t first_p_below(const double* __restrict__ w, d
   return hi;
 }
 
-// ---- exponential variates: 256-layer ziggurat (Marsaglia & Tsang 2000) ----
-// x[1] = r, x[i+1] = -log(v/x[i] + e^{-x[i]}), x[256] = 0, x[0] = v e^{r};
-// f[i] = e^{-x[i]}.  Exact method: ~98.9% of draws cost one multiply.
-constexpr int kZigLayers = 256;
-struct ZigTable {
-  double x[kZigLayers + 1];
-  double f[kZigLayers + 1];
-};
-
 __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
   return static_cast<double>(b >> 11) * 0x1.0p-53;
 }
@@ -161,18 +135,6 @@ __device__ __forceinline__ double exp_inv(Xoshiro& g, const LogTable& T) {
   return -__fma_rn(e, 0x1.62e42fefa39efp-1, T.nlog_inv[i] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * s));
 }
 
-__device__ __forceinline__ double exp_zig(Xoshiro& g, const ZigTable& Z) {
-  for (;;) {
-    const uint64_t b = g.next();
-    const int i = static_cast<int>(b & (kZigLayers - 1));
-    const double x = unit53(b) * Z.x[i];
-    if (x < Z.x[i + 1]) return x;
-    if (i == 0) return Z.x[1] - log(g.open01());  // tail beyond r
-    const double y = Z.f[i] + unit53(g.next()) * (Z.f[i + 1] - Z.f[i]);
-    if (y < exp(-x)) return x;
-  }
-}
-
 // Key of the per-unit stream: a bijection of (u, split) mixed with the seed.
 __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint32_t split) {
   return mix64(seed_mix ^ (static_cast<uint64_t>(u) | (static_cast<uint64_t>(split) << 36)));
@@ -180,9 +142,6 @@ __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint3
 
 enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
-struct CtrTables {
-  ZigTable zig;
-};
 
 #define EMIT_EDGE(ACC, VV) { \
     if (ACC) { \
