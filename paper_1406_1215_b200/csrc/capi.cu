@@ -144,6 +144,7 @@ struct clgen_dev_ctx {
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
+  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 1.0));
   clg::LogTable* logtab = nullptr;  // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
@@ -543,6 +544,7 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   a.lo = lo;
   a.hi = hi;
   c->seed_mix = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
+  a.refill_min = c->ctr_refill_min;
   a.seg = segments(c);
   a.H = c->ctr_H;
   a.hub_units = c->hub_units.as<int64_t>();

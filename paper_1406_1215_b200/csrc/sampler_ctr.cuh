@@ -74,6 +74,7 @@ struct CtrWalkArgs {
   unsigned long long* fold_out;
   unsigned long long* overflow;
   WarpProf prof;
+  int refill_min;  // refill idle lanes only when at least this many are idle
 };
 
 // Segment holding position j (binary search over start[]).
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
 
   for (;;) {
     const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
-    if (need && !drained) {
+    if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
       const int want = __popc(need);
       const int r = __popc(need & lanemask_lt());
       const bool me = (need >> lane) & 1u;
