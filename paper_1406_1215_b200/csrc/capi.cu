@@ -144,7 +144,7 @@ struct clgen_dev_ctx {
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
-  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 1.0));
+  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 8.0));
   clg::LogTable* logtab = nullptr;  // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
