@@ -35,7 +35,7 @@ typedef struct clgen_dev_ctx clgen_dev_ctx;
 
 /* Stream modes for the sampler. */
 #define CLGEN_STREAM_REFERENCE 0 /* per-node xoshiro256++ (rng.hpp:26-69): bit-exact */
-#define CLGEN_STREAM_COUNTER 1   /* counter-based Philox keyed (seed,u,segment,draw) */
+#define CLGEN_STREAM_COUNTER 1   /* keyed xoshiro256+ per (seed,u,split,lane): statistical, GPU-count invariant */
 
 const char* clgen_dev_last_error(void);
 const char* clgen_dev_version(void);

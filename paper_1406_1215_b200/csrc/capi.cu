@@ -94,6 +94,9 @@ struct Scalars {
   unsigned long long ring_head;
   unsigned long long first_bad;
   unsigned long long first_negative;
+  unsigned long long spill;
+  unsigned long long spill_flags;
+  unsigned long long runs;  // flag counter of the spill re-walk (discarded)
   int64_t total;
   double S;
   double fold_final;
@@ -120,6 +123,12 @@ struct clgen_dev_ctx {
   int64_t* flagged = nullptr;  // device, kFlagCap
   int64_t last_flagged = 0;
   DevBuf counts, offsets, tiles, pairs, partials, degree, sources, foldtmp, cum, found;
+  DevBuf slot_cap, soff, scratch, spill;  // single-pass reference-stream materialisation
+  DevBuf run_len;         // run-length table of w (weights.cuh), when runs are long
+  bool has_runs = false;
+  bool use_runs = env_double("CLGEN_RUN_TABLE", 1.0) != 0.0;
+  bool one_pass = env_double("CLGEN_REF_1PASS", 1.0) != 0.0;
+  double slot_sigma = env_double("CLGEN_REF_SLOT_SIGMA", 6.0), slot_const = env_double("CLGEN_REF_SLOT_CONST", 8.0);
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
   // counter stream: weight-class segment table (per weights) and the hub
   // split plan of the last source range
@@ -227,6 +236,7 @@ clg::RefWalkArgs walk_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   clg::RefWalkArgs a;
   std::memset(&a, 0, sizeof a);
   a.w = c->w;
+  a.run_len = c->has_runs ? c->run_len.as<int32_t>() : nullptr;
   a.n = c->n;
   a.S = S;
   a.lo = lo;
@@ -670,9 +680,97 @@ int materialise_ctr(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t
   return CLGEN_OK;
 }
 
-// Two-pass materialisation in the reference's emission order: count pass,
-// decoupled-lookback scan of the per-slot counts, replay pass writing each
-// slot's edges at its scanned offset.
+// Single-pass materialisation in the reference's emission order.  Each slot
+// owns a scratch run sized by ref_slot_cap_kernel (a 6-sigma bound on its
+// edge count); one walk writes the edges there and records the exact counts,
+// a scan of the counts gives the final offsets, ref_compact_kernel moves the
+// runs into place, and the (rare) slots that outgrew their run are re-walked
+// straight into their final offsets.  Output identical to the two-pass path.
+// Returns 1 (nothing launched) when the scratch would not fit in memory.
+int materialise_1pass(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, const int64_t* d_sources,
+                      uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count, int64_t* n_flagged) {
+  int rc;
+  const int64_t m = hi - lo;
+  CUDA_TRY(c->slot_cap.ensure(m * sizeof(int32_t)));
+  CUDA_TRY(c->soff.ensure(m * sizeof(int64_t)));
+  clg::ref_slot_cap_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(c->w, c->n, S, d_sources, lo, m, c->slot_sigma,
+                                                                  c->slot_const, c->slot_cap.as<int32_t>());
+  CUDA_TRY(cudaGetLastError());
+  ++c->launches;
+  if ((rc = launch_scan(c, c->slot_cap.as<int32_t>(), c->soff.as<int64_t>(), m))) return rc;
+  if ((rc = fetch_scalars(c))) return rc;
+  const int64_t scratch_n = c->sc_host->total;
+  const size_t need = static_cast<size_t>(scratch_n > 0 ? scratch_n : 1) * sizeof(uint2);
+  if (need > c->scratch.bytes) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    if (need - c->scratch.bytes > free_b / 2) return 1;
+  }
+  CUDA_TRY(c->scratch.ensure(need));
+  CUDA_TRY(c->spill.ensure(m * sizeof(int64_t)));
+  CUDA_TRY(c->counts.ensure(m * sizeof(int32_t)));
+  CUDA_TRY(c->offsets.ensure(m * sizeof(int64_t)));
+  clg::RefWalkArgs a = walk_args(c, S, lo, hi, seed);
+  a.sources = d_sources;
+  a.counts = c->counts.as<int32_t>();
+  a.offsets = c->soff.as<int64_t>();
+  a.slot_cap = c->slot_cap.as<int32_t>();
+  a.pairs = c->scratch.as<uint2>();
+  a.cap = scratch_n;
+  a.spill = c->spill.as<int64_t>();
+  a.spill_count = &c->sc->spill;
+  if ((rc = launch_walk<clg::kWalkWrite>(c, a))) return rc;
+  if ((rc = launch_scan(c, a.counts, c->offsets.as<int64_t>(), m))) return rc;
+  if ((rc = fetch_scalars(c))) return rc;
+  const int64_t total = c->sc_host->total;
+  const int64_t spilled = static_cast<int64_t>(c->sc_host->spill);
+  const bool dev_out = is_device_ptr(pairs);
+  uint2* d_pairs = reinterpret_cast<uint2*>(pairs);
+  if (!dev_out) {
+    const int64_t stage = total < cap ? total : cap;
+    CUDA_TRY(c->pairs.ensure((stage > 0 ? stage : 1) * sizeof(uint2)));
+    d_pairs = c->pairs.as<uint2>();
+    cap = stage;
+  }
+  clg::ref_compact_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(c->scratch.as<uint2>(), c->soff.as<int64_t>(),
+                                                                 c->slot_cap.as<int32_t>(), a.counts,
+                                                                 c->offsets.as<int64_t>(), m, d_pairs, cap);
+  CUDA_TRY(cudaGetLastError());
+  ++c->launches;
+  if (spilled > 0) {
+    // (source, final offset) of each spilled slot; re-walk them uncapped
+    CUDA_TRY(c->sources.ensure(2 * spilled * sizeof(int64_t)));
+    int64_t* src_list = c->sources.as<int64_t>();
+    int64_t* off_list = src_list + spilled;
+    clg::ref_spill_lists_kernel<<<(spilled + 255) / 256, 256, 0, c->stream>>>(
+        a.spill, &c->sc->spill, d_sources, lo, c->offsets.as<int64_t>(), src_list, off_list);
+    CUDA_TRY(cudaGetLastError());
+    ++c->launches;
+    c->sc_host->queue = 0;
+    CUDA_TRY(cudaMemcpyAsync(&c->sc->queue, &c->sc_host->queue, sizeof(unsigned long long),
+                             cudaMemcpyHostToDevice, c->stream));
+    clg::RefWalkArgs b = walk_args(c, S, 0, spilled, seed);
+    b.sources = src_list;
+    b.offsets = off_list;
+    b.pairs = d_pairs;
+    b.cap = cap;
+    b.flag_count = &c->sc->spill_flags;  // already flagged by the first walk
+    if ((rc = launch_walk<clg::kWalkWrite>(c, b))) return rc;
+  }
+  if (!dev_out && cap > 0)
+    CUDA_TRY(cudaMemcpyAsync(pairs, d_pairs, cap * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  if (count) *count = total;
+  c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);
+  if (n_flagged) *n_flagged = c->last_flagged;
+  if (total > cap)
+    return fail(CLGEN_ERANGE, "create_edges: %lld edges exceed capacity %lld", (long long)total, (long long)cap);
+  return CLGEN_OK;
+}
+
+// Materialisation in the reference's emission order: single pass when the
+// scratch fits (above), else count pass, decoupled-lookback scan of the
+// per-slot counts, replay pass writing each slot's edges at its scanned offset.
 int materialise(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, const int64_t* d_sources,
                 uint64_t seed, uint32_t* pairs, int64_t cap, int64_t* count, int64_t* n_flagged) {
   if (cap < 0 || (cap > 0 && !pairs)) return fail(CLGEN_EINVAL, "create_edges: bad output buffer");
@@ -685,6 +783,11 @@ int materialise(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, const int64_
     if (n_flagged) *n_flagged = 0;
     c->last_flagged = 0;
     return CLGEN_OK;
+  }
+  if (c->one_pass) {
+    rc = materialise_1pass(c, S, lo, hi, d_sources, seed, pairs, cap, count, n_flagged);
+    if (rc != 1) return rc;
+    if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
   }
   CUDA_TRY(c->counts.ensure(m * sizeof(int32_t)));
   CUDA_TRY(c->offsets.ensure(m * sizeof(int64_t)));
@@ -854,6 +957,7 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
     c->w_bytes = bytes;
   }
   c->n = 0;
+  c->has_runs = false;
   c->seg_valid = false;
   c->ctr_lo = c->ctr_hi = -1;
   c->plan_G = 0;
@@ -862,7 +966,8 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
     rc = reset_scalars(c, 0);
     if (rc) return rc;
     const int grid = c->num_sms * 8;
-    clg::check_sorted_kernel<<<grid, 256, 0, c->stream>>>(c->w, n, &c->sc->first_bad, &c->sc->first_negative);
+    clg::check_sorted_kernel<<<grid, 256, 0, c->stream>>>(c->w, n, &c->sc->first_bad, &c->sc->first_negative,
+                                                          &c->sc->runs);
     CUDA_TRY(cudaGetLastError());
     ++c->launches;
     rc = fetch_scalars(c);
@@ -871,6 +976,15 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
       return fail(CLGEN_EINVAL, "weights negative or NaN at position %llu", c->sc_host->first_negative);
     if (c->sc_host->first_bad != ~0ull)
       return fail(CLGEN_EINVAL, "weights unsorted at position %llu", c->sc_host->first_bad);
+    // repeated weights (discrete / constant sequences): run-length table
+    if (c->use_runs && n >= 64 && c->sc_host->runs * 4 <= static_cast<unsigned long long>(n)) {
+      CUDA_TRY(c->run_len.ensure(n * sizeof(int32_t)));
+      const unsigned tiles = static_cast<unsigned>((n + clg::kRunTile - 1) / clg::kRunTile);
+      clg::run_length_kernel<<<tiles, clg::kRunThreads, 0, c->stream>>>(c->w, n, c->run_len.as<int32_t>());
+      CUDA_TRY(cudaGetLastError());
+      ++c->launches;
+      c->has_runs = true;
+    }
   }
   c->n = n;
   // Optional L2 persistence for the hot head of w (candidates land in

@@ -5,8 +5,9 @@
 //   log_fast(x)       x in (0,1): |rel err| <= ~2^-49 (128-entry table of
 //                     reciprocal centres + a degree-7 log1p series on
 //                     |t| <= 2^-8; x >= 15/16 goes through log1m_series)
-//   log1m_fast(p)     log1p(-p), p in (0,1), same bound (degree-15 series
+//   log1m_fast(p)     log1p(-p), p in (0,1), same bound (degree-7/15 series
 //                     for p < 1/16, else log(1-p) with the exact residual)
+//   rcp_fast(x)       1/x to ~2^-52 (float seed + two Newton steps)
 //   div_S(prod)       RN(prod / S) from a correctly rounded 1/S plus one FMA
 //                     correction, certified by an exact residual
 //   accept_ref(r,q,p) r < RN(q / p) decided from the FMA residual q - r p,
@@ -28,8 +29,17 @@ struct LogTable {
 // log1p(-p) for 0 <= p < 1/16: -p * sum_{k=0}^{15} p^k / (k+1)  (trunc < 2^-64 p)
 // Estrin's scheme (dependency depth ~5 instead of 16: this sits on the
 // reference-stream chain's critical path p -> skip -> v -> w[v] -> q = p).
+// For p < 2^-7 the first 8 terms suffice (truncation < p^8 / 9 < 2^-59).
 __device__ __forceinline__ double log1m_series(double p) {
-  const double p2 = p * p, p4 = p2 * p2, p8 = p4 * p4;
+  const double p2 = p * p, p4 = p2 * p2;
+  if (p < 0x1p-7) {
+    const double a0 = __fma_rn(p, 0.5, 1.0);
+    const double a1 = __fma_rn(p, 1.0 / 4.0, 1.0 / 3.0);
+    const double a2 = __fma_rn(p, 1.0 / 6.0, 1.0 / 5.0);
+    const double a3 = __fma_rn(p, 1.0 / 8.0, 1.0 / 7.0);
+    return -p * __fma_rn(p4, __fma_rn(p2, a3, a2), __fma_rn(p2, a1, a0));
+  }
+  const double p8 = p4 * p4;
   // pairs c_k + c_{k+1} p with c_k = 1/(k+1)
   const double a0 = __fma_rn(p, 0.5, 1.0);
   const double a1 = __fma_rn(p, 1.0 / 4.0, 1.0 / 3.0);
@@ -82,6 +92,18 @@ __device__ __forceinline__ double log1m_fast(double p, const LogTable& T) {
   const double t = 1.0 - p;          // rounded; t <= 15/16
   const double e = (1.0 - t) - p;    // exact residual (Fast2Sum, 1 >= p)
   return log_fast(t, T) + e / t;     // log(t + e) = log t + e/t + O((e/t)^2)
+}
+
+// 1/x to ~2^-52 relative: float reciprocal seed + two Newton steps (the
+// skip ratio only needs ~2^-48; __drcp_rn's exact rounding costs ~3x more).
+__device__ __forceinline__ double rcp_fast(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-30 && ax < 1e30)) return __drcp_rn(x);
+  double y = static_cast<double>(__frcp_rn(static_cast<float>(x)));
+  double e = __fma_rn(-x, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-x, y, 1.0);
+  return __fma_rn(y, e, y);
 }
 
 // RN(prod / S) given invS = RN(1/S).  Falls back to __ddiv_rn when the

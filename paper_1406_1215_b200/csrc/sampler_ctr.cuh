@@ -759,8 +759,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             const double incl = warp_incl_scan_f64(pair);
             const double Ta = T0 + (incl - Eb) * inv_c;
             const double Tb = T0 + incl * inv_c;
-            const double r2a = unit53(rng.next_plus());
-            const double r2b = unit53(rng.next_plus());
+            // both acceptance uniforms from one xoshiro256++ draw (all 64
+            // output bits are full quality); 32-bit resolution bounds the
+            // acceptance bias by 2^-33
+            const uint64_t r2bits = rng.next();
+            const double r2a = (static_cast<double>(static_cast<uint32_t>(r2bits >> 32)) + 0.5) * 0x1.0p-32;
+            const double r2b = (static_cast<double>(static_cast<uint32_t>(r2bits)) + 0.5) * 0x1.0p-32;
             const int kla = class_of(Ta, k);
             const int klb = class_of(Tb, kla);
             const uint32_t va = position(Ta, kla);

@@ -17,6 +17,7 @@ enum WalkMode : int { kWalkCount = 0, kWalkWrite = 1, kWalkFold = 2 };
 
 struct RefWalkArgs {
   const double* __restrict__ w;  // non-increasing weights, n entries
+  const int32_t* run_len;        // optional run-length table (weights.cuh): w[v..v+run_len[v]) all equal
   int64_t n;
   double S;
   int64_t lo, hi;                // source slots [lo,hi)
@@ -41,6 +42,12 @@ struct RefWalkArgs {
   int64_t* flagged;              // first flag_cap flagged source ids
   int64_t flag_cap;
   unsigned long long* overflow;  // write mode: slots beyond cap
+  // single-pass write mode: slot i owns [offsets[i], offsets[i] + slot_cap[i]);
+  // counts[i] receives its exact edge count and slots that did not fit are
+  // appended to spill (re-walked later at their final offsets)
+  const int32_t* slot_cap;
+  int64_t* spill;
+  unsigned long long* spill_count;
   WarpProf prof;                 // optional per-warp busy intervals
   // fast math (bit-exact with guarded fallbacks, fastmath.cuh)
   const LogTable* logtab;
@@ -72,7 +79,7 @@ __device__ __forceinline__ int64_t skip_length_ref(double p, double r, bool& amb
 __device__ __forceinline__ int64_t skip_length_fast(double p, double r, bool& amb, const LogTable& T,
                                                     double& lp_p, double& ilp) {
   if (p != lp_p) {
-    ilp = __drcp_rn(log1m_fast(p, T));
+    ilp = rcp_fast(log1m_fast(p, T));
     lp_p = p;
   }
   const double ratio = log_fast(r, T) * ilp;
@@ -108,9 +115,10 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   unsigned long long r_next = 0, r_end = 0;
 
   // lane state
-  int64_t u = -1, slot = 0, j = 0, out_pos = 0;
+  int64_t u = -1, slot = 0, j = 0, out_pos = 0, out_end = 0;
   int32_t cnt = 0;
   double p = 0.0, wu = 0.0, lp_p = -1.0, ilp = 0.0;
+  int64_t run_end = 0;  // w is constant from the last gathered position up to run_end
   bool amb = false;
   Xoshiro rng;
   uint64_t checksum = 0;
@@ -151,10 +159,16 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         cnt = 0;
         amb = false;
         wu = w[u];
-        if (MODE == kWalkWrite) out_pos = a.offsets[slot];
+        if (MODE == kWalkWrite) {
+          out_pos = a.offsets[slot];
+          out_end = a.slot_cap ? out_pos + a.slot_cap[slot] : a.cap;
+        }
+        run_end = 0;
         if (j < n && S > 0.0) {
           rng.seed_key(node_rng_key(a.seed, u));
-          p = fmin(FAST ? div_S(__dmul_rn(wu, w[j]), S, invS) : __ddiv_rn(__dmul_rn(wu, w[j]), S), 1.0);
+          const double wj = w[j];
+          if (a.run_len) run_end = j + a.run_len[j];
+          p = fmin(FAST ? div_S(__dmul_rn(wu, wj), S, invS) : __ddiv_rn(__dmul_rn(wu, wj), S), 1.0);
         } else {
           p = 0.0;
         }
@@ -181,10 +195,19 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
           finish = true;  // edge_skip.cpp:34
         } else {
           v = j + delta;
-          const double prod = __dmul_rn(wu, w[v]);
-          const double q = fmin(FAST ? div_S(prod, S, invS) : __ddiv_rn(prod, S), 1.0);
+          double q;
           const double r2 = rng.open01();
-          accepted = FAST ? accept_ref(r2, q, p) : r2 < __ddiv_rn(q, p);  // edge_skip.cpp:38
+          if (v < run_end) {
+            // same weight as the previous candidate: q = p and q/p = 1 > r2
+            q = p;
+            accepted = true;
+          } else {
+            const double wv = w[v];
+            if (a.run_len) run_end = v + a.run_len[v];
+            const double prod = __dmul_rn(wu, wv);
+            q = fmin(FAST ? div_S(prod, S, invS) : __ddiv_rn(prod, S), 1.0);
+            accepted = FAST ? accept_ref(r2, q, p) : r2 < __ddiv_rn(q, p);  // edge_skip.cpp:38
+          }
           p = q;
           j = v + 1;
         }
@@ -194,9 +217,9 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
     if (accepted) {
       ++cnt;
       if (MODE == kWalkWrite) {
-        if (out_pos < a.cap) {
+        if (out_pos < out_end) {
           a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
-        } else {
+        } else if (!a.slot_cap) {
           atomicAdd(a.overflow, 1ull);
         }
         ++out_pos;
@@ -231,6 +254,10 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
     }
     if (u >= 0 && (finish || !(j < n && p > 0.0))) {
       if (MODE == kWalkCount) a.counts[slot] = cnt;
+      if (MODE == kWalkWrite && a.slot_cap) {
+        a.counts[slot] = cnt;
+        if (out_pos > out_end) a.spill[atomicAdd(a.spill_count, 1ull)] = slot;
+      }
       if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
         atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
       if (amb) {
@@ -253,6 +280,71 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
       atomicAdd(&a.fold_out[0], edges_total);
       atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
     }
+  }
+}
+
+// Per-slot capacity of the single-pass write: the unclamped expected forward
+// degree w_u (S - w_u) / S >= sum_{v>u} min(w_u w_v / S, 1) (sigma_u dropped,
+// so it also bounds every source of a create_edges list) plus k_sigma sigma +
+// k_const (6 and 8 by default).
+__global__ void ref_slot_cap_kernel(const double* __restrict__ w, int64_t n, double S, const int64_t* sources,
+                                    int64_t lo, int64_t m, double k_sigma, double k_const,
+                                    int32_t* __restrict__ cap) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t u = sources ? sources[lo + i] : lo + i;
+    const double wu = w[u];
+    const double e = S > 0.0 ? fmax(wu * (S - wu) / S, 0.0) : 0.0;
+    double c = ceil(e + k_sigma * sqrt(e) + k_const);
+    const double rest = static_cast<double>(n - 1 - u);
+    c = fmin(c, rest);
+    c = fmin(c, 1.0e9);
+    cap[i] = static_cast<int32_t>(c > 0.0 ? c : 0.0);
+  }
+}
+
+// Moves each fitted slot's edges from its scratch run to its final offset.
+// One warp per slot; spilled slots (count > cap) are left to the re-walk.
+__global__ void ref_compact_kernel(const uint2* __restrict__ scratch, const int64_t* __restrict__ soff,
+                                   const int32_t* __restrict__ cap, const int32_t* __restrict__ counts,
+                                   const int64_t* __restrict__ foff, int64_t m, uint2* __restrict__ out,
+                                   int64_t out_cap) {
+  const int lane = lane_id();
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5 << 5; base < m;
+       base += warps * 32) {
+    // lane l loads the metadata of slot base + l; the warp then copies slot by slot
+    const int64_t mine = base + lane;
+    int32_t c = 0, k = 0;
+    int64_t s = 0, f = 0;
+    if (mine < m) {
+      c = counts[mine];
+      k = cap[mine];
+      s = soff[mine];
+      f = foff[mine];
+    }
+    if (c > k) c = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t cl = __shfl_sync(CLG_FULL, c, l);
+      if (cl == 0) continue;
+      const int64_t sl = __shfl_sync(CLG_FULL, s, l);
+      const int64_t fl = __shfl_sync(CLG_FULL, f, l);
+      for (int32_t x = lane; x < cl; x += 32)
+        if (fl + x < out_cap) out[fl + x] = scratch[sl + x];
+    }
+  }
+}
+
+// Spilled slots -> (source, final offset) lists for the re-walk.
+__global__ void ref_spill_lists_kernel(const int64_t* __restrict__ spill, const unsigned long long* spill_count,
+                                       const int64_t* sources, int64_t lo, const int64_t* __restrict__ foff,
+                                       int64_t* __restrict__ src_out, int64_t* __restrict__ off_out) {
+  const int64_t k = static_cast<int64_t>(*spill_count);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t slot = spill[i];
+    src_out[i] = sources ? sources[lo + slot] : lo + slot;
+    off_out[i] = foff[slot];
   }
 }
 

@@ -178,3 +178,52 @@ def test_fast_math_identical_to_reference_expressions(api, port):
     ws = api.make_weight_sequence(w)
     exp, _, _, _ = port.create_edges_range(w, ws.sum_S, 0, w.size, 1002)
     np.testing.assert_array_equal(api.serial_cl(ws, 1002), exp)
+
+
+@pytest.mark.parametrize("env", [
+    {"CLGEN_REF_SLOT_SIGMA": "0", "CLGEN_REF_SLOT_CONST": "0"},   # most slots spill
+    {"CLGEN_REF_SLOT_SIGMA": "1", "CLGEN_REF_SLOT_CONST": "1"},   # some slots spill
+    {"CLGEN_REF_1PASS": "0"},                                      # two-pass path
+])
+def test_materialise_paths_identical(api, port, env, monkeypatch):
+    """Single-pass materialisation (scratch runs + compaction + spill re-walk)
+    and the two-pass path produce the reference's edge list exactly."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    dev = api.Device(0)
+    rng = np.random.default_rng(21)
+    for t in range(6):
+        n = int(rng.integers(1000, 60_000))
+        w = port.synth_powerlaw(n, 2.2 + 0.1 * t, 1.0, 300.0, t)
+        ws = api.make_weight_sequence(w, device=dev)
+        lo, hi = int(rng.integers(0, n // 4)), int(rng.integers(n // 2, n + 1))
+        exp, cnt, _, _ = port.create_edges_range(w, ws.sum_S, lo, hi, 100 + t)
+        np.testing.assert_array_equal(api.create_edges_range(ws, ws.sum_S, lo, hi, 100 + t), exp)
+        out = torch.empty((cnt, 2), dtype=torch.int32, device="cuda")
+        got = api.create_edges_range(ws, ws.sum_S, lo, hi, 100 + t, out=out)
+        np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), exp)
+        src = np.unique(rng.integers(0, n, 500)).astype(np.int64)
+        exp_l, _, _ = port.create_edges(w, ws.sum_S, src, 5 + t)
+        np.testing.assert_array_equal(api.create_edges(ws, ws.sum_S, src, 5 + t), exp_l)
+
+
+@pytest.mark.parametrize("runs", ["1", "0"])
+def test_run_table_bit_exact(api, port, runs, monkeypatch):
+    """Repeated weights (discrete, constant, short and tile-crossing runs):
+    with and without the run-length table the edges equal the oracle's."""
+    monkeypatch.setenv("CLGEN_RUN_TABLE", runs)
+    dev = api.Device(0)
+    rng = np.random.default_rng(33)
+    cases = [np.full(20_000, 7.0),
+             np.sort(rng.integers(1, 40, 50_000).astype(np.float64))[::-1].copy(),
+             np.sort(np.repeat(rng.uniform(1, 300, 700), rng.integers(1, 6000, 700)))[::-1].copy(),
+             np.concatenate([np.full(5000, 900.0), np.full(3, 500.0), np.full(4096 * 3 + 5, 2.0),
+                             np.zeros(100)])]
+    for t, w in enumerate(cases):
+        ws = api.make_weight_sequence(w, device=dev)
+        exp, cnt, cks, _ = port.create_edges_range(w, ws.sum_S, 0, w.size, 40 + t)
+        np.testing.assert_array_equal(api.create_edges_range(ws, ws.sum_S, 0, w.size, 40 + t), exp,
+                                      err_msg=f"case {t}")
+        res = api.stream_range(ws, ws.sum_S, 0, w.size, 40 + t)
+        assert (res.count, res.checksum) == (cnt, cks)
