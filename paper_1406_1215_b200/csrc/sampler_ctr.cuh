@@ -144,42 +144,55 @@ __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint3
 enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
 
-#define EMIT_EDGE(ACC, VV) { \
-    if (ACC) { \
-      ++cnt; \
-      if (MODE == kWalkWrite) { \
-        if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
-        else atomicAdd(a.overflow, 1ull); \
-        ++out_pos; \
-      } else if (MODE == kWalkFold) { \
-        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(VV)); \
-        ++edges_total; \
-        if (a.degree && (VV & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[VV >> a.track_shift], 1u); \
-      } \
-    } \
-    if (MODE == kWalkFold && a.ring) { \
-      const unsigned am = __ballot_sync(CLG_FULL, ACC); \
-      if (am) { \
-        const unsigned kk = __popc(am); \
-        const unsigned rk = __popc(am & lanemask_lt()); \
-        const unsigned long long rem = r_end - r_next; \
-        unsigned long long nb = 0; \
-        if (rem < kk) { \
-          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull); \
-          nb = __shfl_sync(CLG_FULL, nb, 0); \
-        } \
-        if (ACC) { \
-          const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem); \
-          a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VV)); \
-        } \
-        if (rem < kk) { \
-          r_next = nb + (kk - rem); \
-          r_end = nb + 2048ull; \
-        } else { \
-          r_next += kk; \
-        } \
-      } \
-    } \
+// Lane-per-unit emission of up to three edges per lane, in lane order and
+// (A0, A1, A2) order within a lane; one ballot set and one ring reservation.
+#define EMIT_EDGE3(A0, V0, A1, V1, A2, V2) {                                                          \
+    const bool acc_[3] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2)};       \
+    const int64_t vv_[3] = {static_cast<int64_t>(V0), static_cast<int64_t>(V1), static_cast<int64_t>(V2)}; \
+    _Pragma("unroll") for (int e_ = 0; e_ < 3; ++e_) {                                                \
+      if (acc_[e_]) {                                                                                 \
+        ++cnt;                                                                                        \
+        if (MODE == kWalkWrite) {                                                                     \
+          if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(vv_[e_])); \
+          else atomicAdd(a.overflow, 1ull);                                                           \
+          ++out_pos;                                                                                  \
+        } else if (MODE == kWalkFold) {                                                               \
+          checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(vv_[e_]));       \
+          ++edges_total;                                                                              \
+          if (a.degree && (vv_[e_] & ((1ll << a.track_shift) - 1)) == 0)                              \
+            atomicAdd(&a.degree[vv_[e_] >> a.track_shift], 1u);                                       \
+        }                                                                                             \
+      }                                                                                               \
+    }                                                                                                 \
+    if (MODE == kWalkFold && a.ring) {                                                                \
+      const unsigned b0_ = __ballot_sync(CLG_FULL, acc_[0]);                                          \
+      const unsigned b1_ = __ballot_sync(CLG_FULL, acc_[1]);                                          \
+      const unsigned b2_ = __ballot_sync(CLG_FULL, acc_[2]);                                          \
+      if (b0_ | b1_ | b2_) {                                                                          \
+        const unsigned lt_ = lanemask_lt();                                                           \
+        const unsigned kk = __popc(b0_) + __popc(b1_) + __popc(b2_);                                  \
+        unsigned rk = __popc(b0_ & lt_) + __popc(b1_ & lt_) + __popc(b2_ & lt_);                      \
+        const unsigned long long rem = r_end - r_next;                                                \
+        unsigned long long nb = 0;                                                                    \
+        if (rem < kk) {                                                                               \
+          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);                                        \
+          nb = __shfl_sync(CLG_FULL, nb, 0);                                                          \
+        }                                                                                             \
+        _Pragma("unroll") for (int e_ = 0; e_ < 3; ++e_) {                                            \
+          if (acc_[e_]) {                                                                             \
+            const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);                  \
+            a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(vv_[e_])); \
+            ++rk;                                                                                     \
+          }                                                                                           \
+        }                                                                                             \
+        if (rem < kk) {                                                                               \
+          r_next = nb + (kk - rem);                                                                   \
+          r_end = nb + 2048ull;                                                                       \
+        } else {                                                                                      \
+          r_next += kk;                                                                               \
+        }                                                                                             \
+      }                                                                                               \
+    }                                                                                                 \
 }
 
 template <int MODE, int MINB>
@@ -335,8 +348,8 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       continue;
     }
 
-    bool accepted = false;
-    int64_t v = 0;
+    bool accepted = false, accepted1 = false;
+    int64_t v = 0, v1 = 0;
     bool finish = false;
     // resolve the candidate whose weight was requested last iteration
     const bool acc_prev = pend_v >= 0 && pend_r2 < pend_w * pend_f;
@@ -349,44 +362,68 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       if (j >= vend) {
         finish = true;
       } else if (phase == kPhHaz) {
-        // ---- hazard envelope -------------------------------------------
-        T += exp_inv(rng, s_log) * inv_c;
-        if (!(T < em_next)) {
-          if (!(T < s_em[K])) {
-            finish = true;
-          } else {
-            const double bt = T * inv_bucket;
-            const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
-            k = kb > k + 1 ? kb : k + 1;
-            while (!(T < s_em[k + 1])) ++k;
-            em_next = s_em[k + 1];
-            const double z = c_u * s_wf[k], z2 = z * z;
-            gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
-                              z2 * z2 * z2 * (1.0 / 30240.0));
-            thr = s_sure[k] * gk;
-          }
-        }
-        if (!finish) {
-          const int64_t s0 = s_start[k];
-          const double iwf = s_iwf[k];
-          v = s0 + static_cast<int64_t>((T - s_em[k]) * iwf);
-          const int64_t s1 = s_start[k + 1];
-          if (v >= s1) v = s1 - 1;
-          if (v < s0) v = s0;
-          if (v >= vend) {
-            finish = true;
-          } else if (v > prev_v) {  // a position proposed once however many events hit it
-            prev_v = v;
-            const double r2 = unit53(rng.next_plus());
-            if (r2 < thr) {
-              accepted = true;
+        // ---- hazard envelope: two events per iteration -------------------
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (finish) break;
+          bool acc_e = false;
+          int64_t v_e = 0;
+          T += exp_inv(rng, s_log) * inv_c;
+          if (!(T < em_next)) {
+            if (!(T < s_em[K])) {
+              finish = true;
             } else {
-              pend_new = true;
-              pv_new = v;
-              pr2_new = r2;
-              pf_new = gk * iwf;
+              const double bt = T * inv_bucket;
+              const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+              k = kb > k + 1 ? kb : k + 1;
+              while (!(T < s_em[k + 1])) ++k;
+              em_next = s_em[k + 1];
+              const double z = c_u * s_wf[k], z2 = z * z;
+              gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
+                                z2 * z2 * z2 * (1.0 / 30240.0));
+              thr = s_sure[k] * gk;
             }
           }
+          if (!finish) {
+            const int64_t s0 = s_start[k];
+            const double iwf = s_iwf[k];
+            v_e = s0 + static_cast<int64_t>((T - s_em[k]) * iwf);
+            const int64_t s1 = s_start[k + 1];
+            if (v_e >= s1) v_e = s1 - 1;
+            if (v_e < s0) v_e = s0;
+            if (v_e >= vend) {
+              finish = true;
+            } else if (v_e > prev_v) {  // a position proposed once however many events hit it
+              prev_v = v_e;
+              const double r2 = unit53(rng.next_plus());
+              if (r2 < thr) {
+                acc_e = true;
+              } else if (!pend_new) {
+                pend_new = true;
+                pv_new = v_e;
+                pr2_new = r2;
+                pf_new = gk * iwf;
+              } else {  // second uncertain candidate of the iteration (rare): decide now
+                acc_e = r2 < w[v_e] * (gk * iwf);
+              }
+            }
+          }
+          if (e == 0) {
+            accepted = acc_e;
+            v = v_e;
+            // the write pass keeps each unit's edges in position order: an
+            // undecided event 0 (emitted next iteration) ends this iteration
+            if (MODE == kWalkWrite && pend_new) break;
+          } else {
+            accepted1 = acc_e;
+            v1 = v_e;
+          }
+        }
+        // the unit ends this iteration: an outstanding candidate of event 0
+        // must be decided before the lane moves on to another unit
+        if (finish && pend_new) {
+          accepted = pr2_new < w[pv_new] * pf_new;
+          pend_new = false;
         }
       } else if (phase == kPhSat) {
         // ---- saturated band: q = 1, every position is an edge ------------
@@ -445,8 +482,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       pend_f = pf_new;
       pend_w = w[pv_new];
     }
-    EMIT_EDGE(acc_prev, v_prev)
-    EMIT_EDGE(accepted, v)
+    EMIT_EDGE3(acc_prev, v_prev, accepted, v, accepted1, v1)
     if (unit >= 0 && (finish || j >= vend)) {
       if (MODE == kWalkCount) a.counts[unit] = cnt;
       if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
@@ -563,36 +599,43 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     rng.seed_key(mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1)));
 
     // emit helper state per round: (acc, v) -> contiguous output
-// Emit up to two edges per lane (A before B; A lanes before B lanes in the
-// output), one ballot pair and one ring reservation per call.
-#define WARP_EMIT2(ACCA, VA, ACCB, VB)                                                                   \
+// Emit up to four edges per lane in two groups: group 1 = (A0, A1), group
+// 2 = (A2, A3); within a group lane-major (lane l's A0 then A1 before lane
+// l+1's), group 1 before group 2.  One ballot set and one ring reservation
+// per call.
+#define WARP_EMIT4(A0, V0, A1, V1, A2, V2, A3, V3)                                                      \
   {                                                                                                     \
-    const unsigned ba_ = __ballot_sync(CLG_FULL, ACCA);                                                 \
-    const unsigned bb_ = __ballot_sync(CLG_FULL, ACCB);                                                 \
-    if (ba_ | bb_) {                                                                                    \
-      const unsigned kk_ = __popc(ba_) + __popc(bb_);                                                   \
-      const unsigned ra_ = __popc(ba_ & lt_mask) + __popc(bb_ & lt_mask);                               \
-      const unsigned rb_ = ra_ + ((ACCA) ? 1u : 0u);                                                    \
+    const unsigned b0_ = __ballot_sync(CLG_FULL, A0);                                                   \
+    const unsigned b1_ = __ballot_sync(CLG_FULL, A1);                                                   \
+    const unsigned b2_ = __ballot_sync(CLG_FULL, A2);                                                   \
+    const unsigned b3_ = __ballot_sync(CLG_FULL, A3);                                                   \
+    if (b0_ | b1_ | b2_ | b3_) {                                                                        \
+      const unsigned g1_ = __popc(b0_) + __popc(b1_);                                                   \
+      const unsigned kk_ = g1_ + __popc(b2_) + __popc(b3_);                                             \
+      unsigned r_[4];                                                                                   \
+      r_[0] = __popc(b0_ & lt_mask) + __popc(b1_ & lt_mask);                                            \
+      r_[1] = r_[0] + ((A0) ? 1u : 0u);                                                                 \
+      r_[2] = g1_ + __popc(b2_ & lt_mask) + __popc(b3_ & lt_mask);                                      \
+      r_[3] = r_[2] + ((A2) ? 1u : 0u);                                                                 \
+      const bool acc_[4] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2),        \
+                            static_cast<bool>(A3)};                                                     \
+      const uint32_t vv_[4] = {static_cast<uint32_t>(V0), static_cast<uint32_t>(V1),                    \
+                               static_cast<uint32_t>(V2), static_cast<uint32_t>(V3)};                   \
       if (MODE == kWalkWrite) {                                                                         \
-        if (ACCA) {                                                                                     \
-          const int64_t pos_ = out_pos + ra_;                                                           \
-          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VA)); \
-          else atomicAdd(a.overflow, 1ull);                                                             \
-        }                                                                                               \
-        if (ACCB) {                                                                                     \
-          const int64_t pos_ = out_pos + rb_;                                                           \
-          if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VB)); \
-          else atomicAdd(a.overflow, 1ull);                                                             \
+        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                              \
+          if (acc_[e_]) {                                                                               \
+            const int64_t pos_ = out_pos + r_[e_];                                                      \
+            if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), vv_[e_]);            \
+            else atomicAdd(a.overflow, 1ull);                                                           \
+          }                                                                                             \
         }                                                                                               \
         out_pos += kk_;                                                                                 \
       } else if (MODE == kWalkFold) {                                                                   \
-        if (ACCA) {                                                                                     \
-          checksum += mix64(ukey | static_cast<uint64_t>(VA));                                          \
-          if (a.degree && (static_cast<uint32_t>(VA) & tmask) == 0) atomicAdd(&a.degree[(VA) >> a.track_shift], 1u);        \
-        }                                                                                               \
-        if (ACCB) {                                                                                     \
-          checksum += mix64(ukey | static_cast<uint64_t>(VB));                                          \
-          if (a.degree && (static_cast<uint32_t>(VB) & tmask) == 0) atomicAdd(&a.degree[(VB) >> a.track_shift], 1u);        \
+        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                              \
+          if (acc_[e_]) {                                                                               \
+            checksum += mix64(ukey | static_cast<uint64_t>(vv_[e_]));                                   \
+            if (a.degree && (vv_[e_] & tmask) == 0) atomicAdd(&a.degree[vv_[e_] >> a.track_shift], 1u);  \
+          }                                                                                             \
         }                                                                                               \
         edges_total += (lane == 0) ? kk_ : 0;                                                           \
         if (a.ring) {                                                                                   \
@@ -602,13 +645,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             if (lane == 0) nb_ = atomicAdd(a.ring_head, 2048ull);                                       \
             nb_ = __shfl_sync(CLG_FULL, nb_, 0);                                                        \
           }                                                                                             \
-          if (ACCA) {                                                                                   \
-            const unsigned long long pos_ = ra_ < rem_ ? r_next + ra_ : nb_ + (ra_ - rem_);             \
-            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VA)); \
-          }                                                                                             \
-          if (ACCB) {                                                                                   \
-            const unsigned long long pos_ = rb_ < rem_ ? r_next + rb_ : nb_ + (rb_ - rem_);             \
-            a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(VB)); \
+          _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                            \
+            if (acc_[e_]) {                                                                             \
+              const unsigned long long pos_ = r_[e_] < rem_ ? r_next + r_[e_] : nb_ + (r_[e_] - rem_);  \
+              a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), vv_[e_]);               \
+            }                                                                                           \
           }                                                                                             \
           if (rem_ < kk_) {                                                                             \
             r_next = nb_ + (kk_ - rem_);                                                                \
@@ -621,6 +662,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       cnt += kk_;                                                                                       \
     }                                                                                                   \
   }
+#define WARP_EMIT2(ACCA, VA, ACCB, VB) WARP_EMIT4(false, 0u, false, 0u, ACCA, VA, ACCB, VB)
 #define WARP_EMIT(ACC, VV) WARP_EMIT2(ACC, VV, false, 0u)
 
     const uint64_t ukey = static_cast<uint64_t>(u) << 32;
@@ -721,9 +763,8 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
             const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
             const double t = __fma_rn(m, s_log.inv_c[ti], -1.0);
-            double sp = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
-            sp = __fma_rn(t, sp, 1.0 / 5.0);
-            sp = __fma_rn(t, sp, -1.0 / 4.0);
+            // log1p(t), |t| <= 2^-8, to degree 5: absolute error < 2^-50
+            double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
             sp = __fma_rn(t, sp, 1.0 / 3.0);
             sp = __fma_rn(t, sp, -0.5);
             sp = __fma_rn(t, sp, 1.0);
@@ -807,8 +848,8 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
                 accb = r2b < gb * (w[vb] * s_iwf[klb]);
               }
             }
-            if (kDefer) WARP_EMIT2(accpa, pvva, accpb, pvvb)
-            WARP_EMIT2(acca, va, accb, vb)
+            // last round's deferred accepts, then this round's
+            WARP_EMIT4(accpa, pvva, accpb, pvvb, acca, va, accb, vb)
             // carry the last lane's second event into the next round
             if (!__all_sync(CLG_FULL, validb)) {
               if (kDefer) {
@@ -831,6 +872,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     }
 #undef WARP_EMIT
 #undef WARP_EMIT2
+#undef WARP_EMIT4
     if (MODE == kWalkCount && lane == 0) a.counts[unit] = cnt;
     if (MODE == kWalkFold && lane == 0 && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
       atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));

@@ -1,4 +1,4 @@
-#!/bin/bash
-for h in 16 32 64 128; do
-  echo "heavy=$h c3: $(CLGEN_CTR_HEAVY=$h python tools/ref_info.py c3 1e8 counter | tail -1) | c4n1e8: $(CLGEN_CTR_HEAVY=$h python tools/ref_info.py c4 1e8 counter | tail -1)"
+mkdir -p gpurun_out
+for h in 64 96 128 192; do
+  CLGEN_CTR_HEAVY=$h timeout 400 python bench.py --config c4 --no-cpu-baseline --no-e2e --steps 2 --warmup 3 > gpurun_out/sh_$h.log 2>&1
 done
