@@ -144,12 +144,12 @@ __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint3
 enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
 
-// Lane-per-unit emission of up to three edges per lane, in lane order and
-// (A0, A1, A2) order within a lane; one ballot set and one ring reservation.
-#define EMIT_EDGE3(A0, V0, A1, V1, A2, V2) {                                                          \
-    const bool acc_[3] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2)};       \
-    const int64_t vv_[3] = {static_cast<int64_t>(V0), static_cast<int64_t>(V1), static_cast<int64_t>(V2)}; \
-    _Pragma("unroll") for (int e_ = 0; e_ < 3; ++e_) {                                                \
+// Lane-per-unit emission of up to four edges per lane, in lane order and
+// (A0, A1, A2, A3) order within a lane; one ballot set and one ring reservation.
+#define EMIT_EDGE4(A0, V0, A1, V1, A2, V2, A3, V3) {                                                          \
+    const bool acc_[4] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2), static_cast<bool>(A3)}; \
+    const int64_t vv_[4] = {static_cast<int64_t>(V0), static_cast<int64_t>(V1), static_cast<int64_t>(V2), static_cast<int64_t>(V3)}; \
+    _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                                \
       if (acc_[e_]) {                                                                                 \
         ++cnt;                                                                                        \
         if (MODE == kWalkWrite) {                                                                     \
@@ -168,17 +168,18 @@ enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
       const unsigned b0_ = __ballot_sync(CLG_FULL, acc_[0]);                                          \
       const unsigned b1_ = __ballot_sync(CLG_FULL, acc_[1]);                                          \
       const unsigned b2_ = __ballot_sync(CLG_FULL, acc_[2]);                                          \
-      if (b0_ | b1_ | b2_) {                                                                          \
+      const unsigned b3_ = __ballot_sync(CLG_FULL, acc_[3]);                                          \
+      if (b0_ | b1_ | b2_ | b3_) {                                                                    \
         const unsigned lt_ = lanemask_lt();                                                           \
-        const unsigned kk = __popc(b0_) + __popc(b1_) + __popc(b2_);                                  \
-        unsigned rk = __popc(b0_ & lt_) + __popc(b1_ & lt_) + __popc(b2_ & lt_);                      \
+        const unsigned kk = __popc(b0_) + __popc(b1_) + __popc(b2_) + __popc(b3_);                    \
+        unsigned rk = __popc(b0_ & lt_) + __popc(b1_ & lt_) + __popc(b2_ & lt_) + __popc(b3_ & lt_);  \
         const unsigned long long rem = r_end - r_next;                                                \
         unsigned long long nb = 0;                                                                    \
         if (rem < kk) {                                                                               \
           if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);                                        \
           nb = __shfl_sync(CLG_FULL, nb, 0);                                                          \
         }                                                                                             \
-        _Pragma("unroll") for (int e_ = 0; e_ < 3; ++e_) {                                            \
+        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                            \
           if (acc_[e_]) {                                                                             \
             const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);                  \
             a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(vv_[e_])); \
@@ -194,6 +195,11 @@ enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
       }                                                                                               \
     }                                                                                                 \
 }
+
+#ifndef CLG_LANE_EVENTS
+#define CLG_LANE_EVENTS 3
+#endif
+constexpr int kLaneEvents = CLG_LANE_EVENTS;  // hazard events per lane iteration (light units)
 
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
@@ -348,23 +354,24 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       continue;
     }
 
-    bool accepted = false, accepted1 = false;
-    int64_t v = 0, v1 = 0;
+    bool accepted = false, accepted1 = false, accepted2 = false;
+    int64_t v = 0, v1 = 0, v2 = 0;
     bool finish = false;
     // resolve the candidate whose weight was requested last iteration
     const bool acc_prev = pend_v >= 0 && pend_r2 < pend_w * pend_f;
     const int64_t v_prev = pend_v;
     pend_v = -1;
     bool pend_new = false;
+    int pend_slot = -1;
     int64_t pv_new = 0;
     double pr2_new = 0.0, pf_new = 0.0;
     if (unit >= 0) {
       if (j >= vend) {
         finish = true;
       } else if (phase == kPhHaz) {
-        // ---- hazard envelope: two events per iteration -------------------
+        // ---- hazard envelope: kLaneEvents events per iteration -----------
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < kLaneEvents; ++e) {
           if (finish) break;
           bool acc_e = false;
           int64_t v_e = 0;
@@ -411,18 +418,25 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           if (e == 0) {
             accepted = acc_e;
             v = v_e;
-            // the write pass keeps each unit's edges in position order: an
-            // undecided event 0 (emitted next iteration) ends this iteration
-            if (MODE == kWalkWrite && pend_new) break;
-          } else {
+          } else if (e == 1) {
             accepted1 = acc_e;
             v1 = v_e;
+          } else {
+            accepted2 = acc_e;
+            v2 = v_e;
           }
+          if (pend_new && pend_slot < 0) pend_slot = e;
+          // the write pass keeps each unit's edges in position order: an
+          // undecided event (emitted next iteration) ends this iteration
+          if (MODE == kWalkWrite && pend_new) break;
         }
-        // the unit ends this iteration: an outstanding candidate of event 0
-        // must be decided before the lane moves on to another unit
+        // the unit ends this iteration: an outstanding candidate must be
+        // decided before the lane moves on to another unit
         if (finish && pend_new) {
-          accepted = pr2_new < w[pv_new] * pf_new;
+          const bool acc_p = pr2_new < w[pv_new] * pf_new;
+          if (pend_slot == 0) accepted = acc_p;
+          else if (pend_slot == 1) accepted1 = acc_p;
+          else accepted2 = acc_p;
           pend_new = false;
         }
       } else if (phase == kPhSat) {
@@ -482,7 +496,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       pend_f = pf_new;
       pend_w = w[pv_new];
     }
-    EMIT_EDGE3(acc_prev, v_prev, accepted, v, accepted1, v1)
+    EMIT_EDGE4(acc_prev, v_prev, accepted, v, accepted1, v1, accepted2, v2)
     if (unit >= 0 && (finish || j >= vend)) {
       if (MODE == kWalkCount) a.counts[unit] = cnt;
       if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
