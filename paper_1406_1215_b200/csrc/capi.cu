@@ -179,6 +179,12 @@ clg::WarpProf prof_slots(clgen_dev_ctx* c, int grid, bool first) {
   }
   const int warps = grid * 8;
   c->prof_launch.push_back(c->prof_warps);
+  // size for several full-occupancy launches up front: growing the buffer
+  // later would free the slots an earlier launch of this call writes into
+  if (first && c->prof.ensure(static_cast<size_t>(4 * 64 * c->num_sms) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return p;
+  }
   if (c->prof.ensure(static_cast<size_t>(c->prof_warps + warps) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return p;
