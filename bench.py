@@ -181,18 +181,21 @@ def run_reference(args):
     w = workloads.make(args.config, args.n)
     seed = workloads.WORKLOADS[args.config].seed
     ref = CpuReference(w, args.cpu_seconds / 2)
-    vals, last = [], None
+    vals, step_ms, last = [], [], None
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         last = ref.step(seed + i)
         if i >= args.warmup:
             vals.append(last["value"])
+            step_ms.append((time.perf_counter() - t0) * 1e3)
     v = float(np.median(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)),
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {workloads.WORKLOADS[args.config].desc}",
-                   "n": int(w.size)},
+                   "n": int(w.size), "step": "one bounded sample of the workload (cpu_baseline.sample)"},
         "cpu_baseline": {**last, "value": v},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
