@@ -613,6 +613,18 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     rng.seed_key(mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1)));
 
     // emit helper state per round: (acc, v) -> contiguous output
+// Fold-mode work of one emitted edge: checksum, tracked degree, ring store at
+// ring rank R (within this call's reservation: rem_ slots left in the warp's
+// current chunk, then the new chunk nb_).
+#define EMIT_SLOT_FOLD(ACC, V, R)                                                                       \
+  if (ACC) {                                                                                            \
+    checksum += mix64(ukey | static_cast<uint64_t>(V));                                                 \
+    if (a.degree && ((V) & tmask) == 0) atomicAdd(&a.degree[(V) >> a.track_shift], 1u);                \
+    if (a.ring) {                                                                                       \
+      const unsigned long long pos_ = (R) < rem_ ? r_next + (R) : nb_ + ((R) - rem_);                   \
+      a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), (V));                           \
+    }                                                                                                   \
+  }
 // Emit up to four edges per lane in two groups: group 1 = (A0, A1), group
 // 2 = (A2, A3); within a group lane-major (lane l's A0 then A1 before lane
 // l+1's), group 1 before group 2.  One ballot set and one ring reservation
@@ -645,26 +657,26 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
         }                                                                                               \
         out_pos += kk_;                                                                                 \
       } else if (MODE == kWalkFold) {                                                                   \
-        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                              \
-          if (acc_[e_]) {                                                                               \
-            checksum += mix64(ukey | static_cast<uint64_t>(vv_[e_]));                                   \
-            if (a.degree && (vv_[e_] & tmask) == 0) atomicAdd(&a.degree[vv_[e_] >> a.track_shift], 1u);  \
-          }                                                                                             \
-        }                                                                                               \
         edges_total += (lane == 0) ? kk_ : 0;                                                           \
+        unsigned rem_ = 0;                                                                              \
+        unsigned long long nb_ = 0;                                                                     \
         if (a.ring) {                                                                                   \
-          const unsigned rem_ = static_cast<unsigned>(r_end - r_next);                                  \
-          unsigned long long nb_ = 0;                                                                   \
+          rem_ = static_cast<unsigned>(r_end - r_next);                                                 \
           if (rem_ < kk_) {                                                                             \
             if (lane == 0) nb_ = atomicAdd(a.ring_head, 2048ull);                                       \
             nb_ = __shfl_sync(CLG_FULL, nb_, 0);                                                        \
           }                                                                                             \
-          _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                            \
-            if (acc_[e_]) {                                                                             \
-              const unsigned long long pos_ = r_[e_] < rem_ ? r_next + r_[e_] : nb_ + (r_[e_] - rem_);  \
-              a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), vv_[e_]);               \
-            }                                                                                           \
-          }                                                                                             \
+        }                                                                                               \
+        /* warp-uniform group branches: a group without edges costs nothing */                          \
+        if (g1_) {                                                                                      \
+          EMIT_SLOT_FOLD(acc_[0], vv_[0], r_[0])                                                        \
+          EMIT_SLOT_FOLD(acc_[1], vv_[1], r_[1])                                                        \
+        }                                                                                               \
+        if (kk_ != g1_) {                                                                               \
+          EMIT_SLOT_FOLD(acc_[2], vv_[2], r_[2])                                                        \
+          EMIT_SLOT_FOLD(acc_[3], vv_[3], r_[3])                                                        \
+        }                                                                                               \
+        if (a.ring) {                                                                                   \
           if (rem_ < kk_) {                                                                             \
             r_next = nb_ + (kk_ - rem_);                                                                \
             r_end = nb_ + 2048ull;                                                                      \
@@ -887,6 +899,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
 #undef WARP_EMIT
 #undef WARP_EMIT2
 #undef WARP_EMIT4
+#undef EMIT_SLOT_FOLD
     if (MODE == kWalkCount && lane == 0) a.counts[unit] = cnt;
     if (MODE == kWalkFold && lane == 0 && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
       atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
