@@ -202,6 +202,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def write_only_gbs(torch, stream) -> float | None:
+    """Write-only HBM bandwidth on this box: best of 10
+    fills of a 4 GiB buffer, CUDA events on the bench stream, outside the
+    timed region.  Reported beside the copy-bandwidth peak."""
+    try:
+        with torch.cuda.stream(stream):
+            buf = torch.empty(1 << 29, dtype=torch.int64, device="cuda")
+            best = None
+            for _ in range(10):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                buf.fill_(1)
+                e1.record(stream)
+                e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = ms if best is None or ms < best else best
+            nbytes = buf.numel() * 8
+            del buf
+        return nbytes / (best / 1e3) / 1e9
+    except Exception:
+        return None
+
+
 # --------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -322,6 +346,7 @@ def run_ours(args):
         e2e = runtime.e2e_measure(args, w_host, world, rank, local, lo, hi, seed, materialise)
 
     hbm, peak_kind = peaks()
+    write_gbs = write_only_gbs(torch, stream) if rank == 0 else None
     my_edges = edges_total // args.steps
     achieved = my_edges * BYTES_PER_EDGE / (kern_step / 1e3) / 1e9
     traffic = runtime.ncu_traffic(args.config, args.mode)
@@ -352,6 +377,8 @@ def run_ours(args):
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)",
                          "kernel_ms": kern_step,
+                         "write_only_gbs": write_gbs,
+                         "frac_of_write_only": (achieved / write_gbs) if write_gbs else None,
                          "algorithmic_bytes": f"{BYTES_PER_EDGE} B/edge x {my_edges} edges"},
             "cpu_baseline": cpu,
             "e2e": e2e,
