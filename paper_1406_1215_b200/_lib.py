@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libclgen_b200.so")
+LIB_PATH = os.environ.get("CLGEN_LIB") or os.path.join(HERE, "libclgen_b200.so")  # CLGEN_LIB: A/B tooling only
 
 CLGEN_OK = 0
 CLGEN_EINVAL = -1

@@ -134,6 +134,7 @@ struct clgen_dev_ctx {
   // split plan of the last source range
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
   int seg_K = 0;
+  int seg_depth = 64;  // bucket lookup depth (segment_buckets_kernel)
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
@@ -448,9 +449,15 @@ int ensure_segments(clgen_dev_ctx* c) {
       sg.K = K;
       clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
       clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>());
-      clg::segment_buckets_kernel<<<clg::kBuckets / 256, 256, 0, c->stream>>>(sg, c->seg_bucket.as<unsigned short>());
+      CUDA_TRY(cudaMemsetAsync(&c->sc->total, 0, sizeof(int64_t), c->stream));
+      clg::segment_buckets_kernel<<<clg::kBuckets / 256, 256, 0, c->stream>>>(
+          sg, c->seg_bucket.as<unsigned short>(), reinterpret_cast<int*>(&c->sc->total));
       c->launches += 3;
       CUDA_TRY(cudaGetLastError());
+      int depth = 0;
+      CUDA_TRY(cudaMemcpyAsync(&depth, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      c->seg_depth = depth;
       c->seg_valid = true;
       return CLGEN_OK;
     }
@@ -461,7 +468,7 @@ int ensure_segments(clgen_dev_ctx* c) {
 clg::Segments segments(clgen_dev_ctx* c) {
   return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
                        c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
-                       c->seg_bucket.as<unsigned short>()};
+                       c->seg_bucket.as<unsigned short>(), c->seg_depth};
 }
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected

@@ -42,10 +42,12 @@ struct Segments {
   const double* em;      // K+1 envelope-mass prefix: em[k+1] = em[k] + wfirst[k] * len_k
   const double* invwf;   // 1 / wfirst[k] (0 for a zero class)
   int K;
-  const unsigned short* bucket;  // kBuckets entries: class holding envelope mass b * em[K] / kBuckets
+  const unsigned short* bucket;  // kBuckets entries: a lower bound of the class of any T in bucket b
+  int depth;  // max over buckets of (classes a bucket can reach) - 1: the class of T is within
+              // [bucket[b], bucket[b] + depth]
 };
 
-constexpr int kBuckets = 4096;
+constexpr int kBuckets = 8192;
 
 constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA (static smem < 48 KB)
 constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
@@ -521,12 +523,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
 }
 
 // ---- warp-cooperative processing of heavy units --------------------------
-// All 32 lanes work on one unit: round r, lane l takes Poisson event 32r+l of
-// the unit's hazard process (a warp prefix sum of exponentials), so positions
-// come out sorted across lanes; duplicates are adjacent (neighbour shuffle),
-// accepted edges are compacted by one ballot and stored contiguously.  Lane l
-// draws from its own keyed stream (unit key, lane), so the draws and hence
-// the edges are a deterministic function of (seed, u, split).
+// All 32 lanes work on one unit: round r, lane l takes Poisson events 64r+2l
+// and 64r+2l+1 of the unit's hazard process (a warp prefix sum of
+// exponential pairs), so positions come out sorted across lanes; duplicates
+// are adjacent (neighbour shuffle).  Lane l draws from its own keyed stream
+// (unit key, lane), so the draws and hence the edges are a deterministic
+// function of (seed, u, split) — the same in the count, write and fold modes.
 __device__ __forceinline__ double warp_incl_scan_f64(double x) {
   const int lane = lane_id();
 #pragma unroll
@@ -542,44 +544,161 @@ __device__ __forceinline__ double bern_gk(double inv_kappa, double z) {
   return inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) + z2 * z2 * z2 * (1.0 / 30240.0));
 }
 
+// Exp(1) by inversion from the top 53 bits of x, E = -log(U),
+// U = (x>>11 + 1/2) 2^-53 in (0,1): table log (128 entries) + degree-5
+// log1p, absolute error < 2^-50 (statistically exact).
+__device__ __forceinline__ double exp_bits(uint64_t x, const LogTable& T) {
+  const double u = __dmul_rn(static_cast<double>(x >> 11) + 0.5, 0x1.0p-53);
+  const long long bx = __double_as_longlong(u);
+  const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
+  const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
+  const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double t = __fma_rn(m, T.inv_c[ti], -1.0);
+  double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
+  sp = __fma_rn(t, sp, 1.0 / 3.0);
+  sp = __fma_rn(t, sp, -0.5);
+  sp = __fma_rn(t, sp, 1.0);
+  const double e = static_cast<double>(ex);
+  return -__fma_rn(e, 0x1.62e42fefa39efp-1, T.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
+}
+
+// Bernoulli(a) from a lazily refined uniform R = (h + R')/2048: the 11 bits h
+// come with the event's exponential draw (its low bits), R' (53 bits) is
+// drawn only when h alone cannot decide (probability 1/2048 per uncertain
+// test) from a hash of the event's identity, so the decision does not
+// depend on when it is taken (the fold mode defers it by one round).
+__device__ __forceinline__ bool lazy_accept(uint32_t h, double a, uint64_t key, uint32_t id) {
+  const double s = a * 2048.0;  // exact scaling
+  if (static_cast<double>(h + 1u) <= s) return true;
+  if (static_cast<double>(h) >= s) return false;
+  const uint64_t r = mix64(key + 0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(id) + 1ull));
+  return unit53(r) < s - static_cast<double>(h);  // s - h exact (Sterbenz)
+}
+
+// Fold-mode sink of one warp: checksum, edge count, tracked degrees and the
+// ring store of every emitted edge.  Each warp of the launch owns a private
+// circular segment of the ring (no reservation atomics): slot = base +
+// (emitted-by-this-warp mod segment).  emit2 takes up to two edges per lane,
+// slots assigned lane-major by one ballot pair.
+struct FoldSink {
+  uint64_t checksum;
+  unsigned long long edges;
+  uint2* seg;       // this warp's ring segment (nullptr: no ring)
+  uint32_t smask;   // segment length - 1
+  uint32_t wpos;    // edges this warp has written (warp-uniform)
+
+  __device__ __forceinline__ void init(const CtrWalkArgs& a) {
+    checksum = 0;
+    edges = 0;
+    seg = nullptr;
+    smask = 0;
+    wpos = 0;
+    if (a.ring) {
+      const unsigned nw = gridDim.x * (blockDim.x >> 5);
+      const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+      const int lcap = 63 - __clzll(static_cast<long long>(a.ring_mask + 1ull));
+      const int lnw = nw > 1 ? 32 - __clz(nw - 1) : 0;
+      int sl = lcap - lnw;
+      sl = sl < 5 ? 5 : (sl > 20 ? 20 : sl);
+      if (sl > lcap) sl = lcap;
+      smask = (1u << sl) - 1u;
+      seg = a.ring + ((static_cast<unsigned long long>(gw) << sl) & a.ring_mask);
+    }
+  }
+
+  __device__ __forceinline__ void one(const CtrWalkArgs& a, uint32_t u, uint32_t v, uint32_t tmask, uint32_t r) {
+    checksum += mix64((static_cast<uint64_t>(u) << 32) | v);
+    if (a.degree && (v & tmask) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
+    if (seg) seg[(wpos + r) & smask] = make_uint2(u, v);
+  }
+
+  __device__ __forceinline__ void emit2(const CtrWalkArgs& a, uint32_t u, uint32_t tmask, unsigned lt, int lane,
+                                        bool c0, uint32_t v0, bool c1, uint32_t v1) {
+    const unsigned b0 = __ballot_sync(CLG_FULL, c0), b1 = __ballot_sync(CLG_FULL, c1);
+    if ((b0 | b1) == 0u) return;
+    const unsigned r0 = __popc(b0 & lt) + __popc(b1 & lt);
+    edges += (c0 ? 1u : 0u) + (c1 ? 1u : 0u);
+    if (c0) one(a, u, v0, tmask, r0);
+    if (c1) one(a, u, v1, tmask, r0 + (c0 ? 1u : 0u));
+    wpos += __popc(b0) + __popc(b1);
+  }
+
+  // warp totals into fold_out[0..1]
+  __device__ __forceinline__ void finish(const CtrWalkArgs& a, int lane) {
+    const uint64_t c = warp_sum_u64(checksum);
+    const uint64_t e = warp_sum_u64(edges);
+    if (lane == 0) {
+      atomicAdd(&a.fold_out[0], static_cast<unsigned long long>(e));
+      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(c));
+    }
+  }
+};
+
+constexpr int kSideCap = 128;  // per-warp staging of deferred accepts (fold mode)
+
+// Class record staged in shared memory: everything an event needs to map its
+// envelope mass T to a position in class k (two 16-byte loads).
+struct __align__(16) ClassRec {
+  double em;    // envelope mass before class k
+  double iwf;   // 1 / wfirst[k] (0 for a zero class)
+  uint32_t s0;  // first node of the class (node ids < 2^32 in the counter stream)
+  uint32_t s1;  // one past the last node
+  double wf;    // wfirst[k]
+};
+
+// Class holding position j (binary search over the records).
+__device__ __forceinline__ int rec_of(const ClassRec* r, int K, int64_t j) {
+  int a = 0, b = K;
+  while (b - a > 1) {
+    const int m = (a + b) >> 1;
+    if (static_cast<int64_t>(r[m].s0) <= j) a = m; else b = m;
+  }
+  return a;
+}
+
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                           const LogTable* __restrict__ logtab, uint64_t seed_mix,
                                                           int64_t U_heavy, unsigned long long* queue_heavy) {
-  __shared__ int64_t s_start[kSegSmemMax + 1];
-  __shared__ double s_em[kSegSmemMax + 1];
-  __shared__ double s_wf[kSegSmemMax];
-  __shared__ double s_iwf[kSegSmemMax];
-  __shared__ double s_sure[kSegSmemMax];
+  __shared__ ClassRec s_rec[kSegSmemMax + 2];
   __shared__ LogTable s_log;
+  __shared__ unsigned short s_bucket[kBuckets];
+  __shared__ uint32_t s_side[256 / 32][kSideCap];
   const int K = a.seg.K;
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
-    s_start[i] = a.seg.start[i];
-    s_em[i] = a.seg.em[i];
-    if (i < K) {
-      s_wf[i] = a.seg.wfirst[i];
-      s_iwf[i] = a.seg.invwf[i];
-      s_sure[i] = a.seg.sure[i];
+    ClassRec r;
+    r.em = a.seg.em[i];
+    r.iwf = i < K ? a.seg.invwf[i] : 0.0;
+    r.s0 = static_cast<uint32_t>(a.seg.start[i]);
+    r.s1 = i < K ? static_cast<uint32_t>(a.seg.start[i + 1]) : r.s0;
+    r.wf = i < K ? a.seg.wfirst[i] : 0.0;
+    s_rec[i] = r;
+    if (i == K) {  // sentinel past the end: no T reaches it
+      r.em = __longlong_as_double(0x7ff0000000000000LL);
+      r.iwf = 0.0;
+      r.wf = 0.0;
+      s_rec[K + 1] = r;
     }
   }
   for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
     s_log.inv_c[i] = logtab->inv_c[i];
     s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
-  __shared__ unsigned short s_bucket[kBuckets];
   for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
-  const double inv_bucket = static_cast<double>(kBuckets) / s_em[K];
+  const double inv_bucket = static_cast<double>(kBuckets) / s_rec[K].em;
+  const double* __restrict__ g_sure = a.seg.sure;
 
   const int lane = lane_id();
+  uint32_t* side = s_side[threadIdx.x >> 5];
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const unsigned lt_mask = lanemask_lt();
   const double* __restrict__ w = a.w;
   const double S = a.S;
-  const double em_end = s_em[K];
-  unsigned long long r_next = 0, r_end = 0;  // ring reservation (fold mode)
-  uint64_t checksum = 0;
-  unsigned long long edges_total = 0;
+  const double em_end = s_rec[K].em;
+  const uint32_t tmask = (1u << a.track_shift) - 1u;
+  FoldSink fs;
+  fs.init(a);
   Xoshiro rng;
 
   for (;;) {
@@ -607,92 +726,66 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       vend = a.n;
     }
     const double wu = w[u];
+    const uint32_t u32 = static_cast<uint32_t>(u);
     int64_t out_pos = MODE == kWalkWrite ? a.offsets[unit] : 0;
     int32_t cnt = 0;
     // lane streams: key(u, split) mixed with the lane
-    rng.seed_key(mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1)));
+    const uint64_t lkey = mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1));
+    rng.seed_key(lkey);
 
-    // emit helper state per round: (acc, v) -> contiguous output
-// Fold-mode work of one emitted edge: checksum, tracked degree, ring store at
-// ring rank R (within this call's reservation: rem_ slots left in the warp's
-// current chunk, then the new chunk nb_).
-#define EMIT_SLOT_FOLD(ACC, V, R)                                                                       \
-  if (ACC) {                                                                                            \
-    checksum += mix64(ukey | static_cast<uint64_t>(V));                                                 \
-    if (a.degree && ((V) & tmask) == 0) atomicAdd(&a.degree[(V) >> a.track_shift], 1u);                \
-    if (a.ring) {                                                                                       \
-      const unsigned long long pos_ = (R) < rem_ ? r_next + (R) : nb_ + ((R) - rem_);                   \
-      a.ring[pos_ & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), (V));                           \
-    }                                                                                                   \
-  }
-// Emit up to four edges per lane in two groups: group 1 = (A0, A1), group
-// 2 = (A2, A3); within a group lane-major (lane l's A0 then A1 before lane
-// l+1's), group 1 before group 2.  One ballot set and one ring reservation
-// per call.
-#define WARP_EMIT4(A0, V0, A1, V1, A2, V2, A3, V3)                                                      \
-  {                                                                                                     \
-    const unsigned b0_ = __ballot_sync(CLG_FULL, A0);                                                   \
-    const unsigned b1_ = __ballot_sync(CLG_FULL, A1);                                                   \
-    const unsigned b2_ = __ballot_sync(CLG_FULL, A2);                                                   \
-    const unsigned b3_ = __ballot_sync(CLG_FULL, A3);                                                   \
-    if (b0_ | b1_ | b2_ | b3_) {                                                                        \
-      const unsigned g1_ = __popc(b0_) + __popc(b1_);                                                   \
-      const unsigned kk_ = g1_ + __popc(b2_) + __popc(b3_);                                             \
-      unsigned r_[4];                                                                                   \
-      r_[0] = __popc(b0_ & lt_mask) + __popc(b1_ & lt_mask);                                            \
-      r_[1] = r_[0] + ((A0) ? 1u : 0u);                                                                 \
-      r_[2] = g1_ + __popc(b2_ & lt_mask) + __popc(b3_ & lt_mask);                                      \
-      r_[3] = r_[2] + ((A2) ? 1u : 0u);                                                                 \
-      const bool acc_[4] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2),        \
-                            static_cast<bool>(A3)};                                                     \
-      const uint32_t vv_[4] = {static_cast<uint32_t>(V0), static_cast<uint32_t>(V1),                    \
-                               static_cast<uint32_t>(V2), static_cast<uint32_t>(V3)};                   \
-      if (MODE == kWalkWrite) {                                                                         \
-        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                              \
-          if (acc_[e_]) {                                                                               \
-            const int64_t pos_ = out_pos + r_[e_];                                                      \
-            if (pos_ < a.cap) a.pairs[pos_] = make_uint2(static_cast<uint32_t>(u), vv_[e_]);            \
-            else atomicAdd(a.overflow, 1ull);                                                           \
-          }                                                                                             \
-        }                                                                                               \
-        out_pos += kk_;                                                                                 \
-      } else if (MODE == kWalkFold) {                                                                   \
-        edges_total += (lane == 0) ? kk_ : 0;                                                           \
-        unsigned rem_ = 0;                                                                              \
-        unsigned long long nb_ = 0;                                                                     \
-        if (a.ring) {                                                                                   \
-          rem_ = static_cast<unsigned>(r_end - r_next);                                                 \
-          if (rem_ < kk_) {                                                                             \
-            if (lane == 0) nb_ = atomicAdd(a.ring_head, 2048ull);                                       \
-            nb_ = __shfl_sync(CLG_FULL, nb_, 0);                                                        \
-          }                                                                                             \
-        }                                                                                               \
-        /* warp-uniform group branches: a group without edges costs nothing */                          \
-        if (g1_) {                                                                                      \
-          EMIT_SLOT_FOLD(acc_[0], vv_[0], r_[0])                                                        \
-          EMIT_SLOT_FOLD(acc_[1], vv_[1], r_[1])                                                        \
-        }                                                                                               \
-        if (kk_ != g1_) {                                                                               \
-          EMIT_SLOT_FOLD(acc_[2], vv_[2], r_[2])                                                        \
-          EMIT_SLOT_FOLD(acc_[3], vv_[3], r_[3])                                                        \
-        }                                                                                               \
-        if (a.ring) {                                                                                   \
-          if (rem_ < kk_) {                                                                             \
-            r_next = nb_ + (kk_ - rem_);                                                                \
-            r_end = nb_ + 2048ull;                                                                      \
-          } else {                                                                                      \
-            r_next += kk_;                                                                              \
-          }                                                                                             \
-        }                                                                                               \
-      }                                                                                                 \
-      cnt += kk_;                                                                                       \
-    }                                                                                                   \
-  }
-#define WARP_EMIT2(ACCA, VA, ACCB, VB) WARP_EMIT4(false, 0u, false, 0u, ACCA, VA, ACCB, VB)
-#define WARP_EMIT(ACC, VV) WARP_EMIT2(ACC, VV, false, 0u)
+    // emission of up to two edges per lane, lane-major (c0 before c1)
+    auto emit2 = [&](bool c0, uint32_t v0, bool c1, uint32_t v1) {
+      if (MODE == kWalkFold) {
+        fs.emit2(a, u32, tmask, lt_mask, lane, c0, v0, c1, v1);
+      } else {
+        const unsigned b0 = __ballot_sync(CLG_FULL, c0), b1 = __ballot_sync(CLG_FULL, c1);
+        const unsigned kk = __popc(b0) + __popc(b1);
+        if (MODE == kWalkWrite && kk) {
+          const unsigned r0 = __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
+          if (c0) {
+            const int64_t p = out_pos + r0;
+            if (p < a.cap) a.pairs[p] = make_uint2(u32, v0); else atomicAdd(a.overflow, 1ull);
+          }
+          if (c1) {
+            const int64_t p = out_pos + r0 + (c0 ? 1 : 0);
+            if (p < a.cap) a.pairs[p] = make_uint2(u32, v1); else atomicAdd(a.overflow, 1ull);
+          }
+          out_pos += kk;
+        }
+        cnt += kk;
+      }
+    };
+    // fold mode: deferred accepts are staged per warp in shared memory and
+    // folded 32 at a time (one per lane)
+    unsigned side_n = 0;
+    auto side_push = [&](bool c0, uint32_t v0, bool c1, uint32_t v1) {
+      const unsigned b0 = __ballot_sync(CLG_FULL, c0), b1 = __ballot_sync(CLG_FULL, c1);
+      if ((b0 | b1) == 0u) return;
+      const unsigned r0 = side_n + __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
+      if (c0) side[r0] = v0;
+      if (c1) side[r0 + (c0 ? 1u : 0u)] = v1;
+      side_n += __popc(b0) + __popc(b1);  // <= 31 + 64
+      while (side_n >= 32) {
+        __syncwarp();
+        const uint32_t v = side[lane], vn = side[32 + lane], vm = side[64 + lane];
+        __syncwarp();
+        side[lane] = vn;  // keep the rest (< 64 entries)
+        side[32 + lane] = vm;
+        fs.emit2(a, u32, tmask, lt_mask, lane, true, v, false, 0u);
+        side_n -= 32;
+      }
+    };
+    auto side_flush = [&]() {
+      if (side_n > 0) {  // < 32 entries left
+        __syncwarp();
+        const bool c = static_cast<unsigned>(lane) < side_n;
+        const uint32_t v = side[lane];
+        fs.emit2(a, u32, tmask, lt_mask, lane, c, v, false, 0u);
+        side_n = 0;
+      }
+    };
+    const unsigned long long e_unit = fs.edges;
 
-    const uint64_t ukey = static_cast<uint64_t>(u) << 32;
-    const uint32_t tmask = (1u << a.track_shift) - 1u;
     if (j < vend && S > 0.0 && wu > 0.0) {
       const double y0 = pbar_of(wu, w[j], S);
       int64_t vB = j, vsat = j;
@@ -703,8 +796,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       // ---- saturated band: every position is an edge (cooperative) ----
       for (int64_t p0 = j; p0 < vsat; p0 += 32) {
         const int64_t v = p0 + lane;
-        const bool acc = v < vsat;
-        WARP_EMIT(acc, v)
+        emit2(v < vsat, static_cast<uint32_t>(v), false, 0u);
       }
       // ---- heavy band [vsat, vB): per class a Bernoulli(pbar_k) process,
       // cooperatively: lane i draws a geometric gap, an integer warp prefix
@@ -712,11 +804,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       // next class (memoryless) ----
       if (vsat < vB) {
         int64_t jj = vsat;
-        int k = seg_of_s(s_start, K, jj);
+        int k = rec_of(s_rec, K, jj);
         while (jj < vB) {
-          while (s_start[k + 1] <= jj) ++k;
-          const int64_t seg_hi = imin64(s_start[k + 1], vB);
-          const double wf = s_wf[k];
+          while (static_cast<int64_t>(s_rec[k + 1].s0) <= jj) ++k;
+          const int64_t seg_hi = imin64(static_cast<int64_t>(s_rec[k + 1].s0), vB);
+          const double wf = s_rec[k].wf;
           const double pb = fmin(pbar_of(wu, wf, S), 1.0);
           if (pb >= 1.0) {
             // envelope 1: every position is a candidate, accepted with q
@@ -727,12 +819,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
                 const double q = pbar_of(wu, w[v], S);
                 acc = q >= 1.0 || unit53(rng.next_plus()) < q;
               }
-              WARP_EMIT(acc, v)
+              emit2(acc, static_cast<uint32_t>(v), false, 0u);
             }
             jj = seg_hi;
           } else {
             const double imu = 1.0 / -log1p(-pb);  // geometric gap: floor(E / mu) + 1
-            const double sure = s_sure[k];
+            const double sure = g_sure[k];
             for (;;) {
               const double x = unit53(rng.next_plus()) + 0x1.0p-54;  // (0,1)
               const double ratio = -log(x) * imu;
@@ -745,7 +837,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
                 const double r2 = unit53(rng.next_plus());
                 acc = r2 < sure || r2 * wf < w[v];
               }
-              WARP_EMIT(acc, v)
+              emit2(acc, static_cast<uint32_t>(v), false, 0u);
               if (!__all_sync(CLG_FULL, valid)) break;
               jj = __shfl_sync(CLG_FULL, v, 31) + 1;
               if (jj >= seg_hi) break;
@@ -758,8 +850,8 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
       // ---- hazard envelope [vB, vend), cooperative rounds ----
       // Node ids are < 2^32 here (n <= 2^32 - 1, checked by set_weights).
       if (vB < vend) {
-        int k = seg_of_s(s_start, K, vB);
-        const double ymax = pbar_of(wu, s_wf[k], S);
+        int k = rec_of(s_rec, K, vB);
+        const double ymax = pbar_of(wu, s_rec[k].wf, S);
         if (ymax > 0.0) {
           // kappa = -log(1-y)/y = sum_k y^k/(k+1) (y < (1+eps)/16: 16 terms
           // leave < 1e-19); reciprocals by one rcp each
@@ -769,73 +861,74 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
           const double c_u = kappa * (wu / S);
           const double inv_c = __drcp_rn(c_u);
           const double inv_kappa = __drcp_rn(kappa);
-          double T0 = s_em[k] + s_wf[k] * static_cast<double>(vB - s_start[k]);
+          double T0 = s_rec[k].em + s_rec[k].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[k].s0));
           uint32_t prev_v = static_cast<uint32_t>(vB - 1);
           const uint32_t vend32 = static_cast<uint32_t>(vend);
-          // lane i holds the acceptance factor of class kw + i
+          // Acceptance of a candidate in class k: R < (w_v / wfirst_k) g_k,
+          // g_k = (1/kappa) z/(1-e^-z), z = c_u wfirst_k.  Lane i of the
+          // window holds class kw + i: g_k and the sure threshold
+          // hs_k = floor(sure_k g_k 2^11) (R < hs_k / 2^11 accepts without
+          // reading w_v; R's top 11 bits come with the event's draw).
           int kw = k;
-          double g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
+          double g_lane = 0.0;
+          uint32_t hs_lane = 0;
+          auto refresh = [&]() {
+            const int kc = kw + lane;
+            if (kc < K) {
+              g_lane = bern_gk(inv_kappa, c_u * s_rec[kc].wf);
+              hs_lane = static_cast<uint32_t>((__ldg(g_sure + kc) * g_lane) * 2048.0);
+            } else {
+              g_lane = 0.0;
+              hs_lane = 0;
+            }
+          };
+          refresh();
           // count/fold modes resolve an uncertain accept one round later (its
           // w[v] load overlaps the next round); the ordered write pass cannot
           constexpr bool kDefer = MODE != kWalkWrite;
           bool penda = false, pendb = false;
-          uint32_t pva = 0, pvb = 0;
-          double pr2a = 0.0, pfa = 0.0, pwa = 0.0, pr2b = 0.0, pfb = 0.0, pwb = 0.0;
-          // Exp(1) by inversion with the shared log table
-          auto exp1 = [&]() -> double {
-            const double x = __dmul_rn(static_cast<double>(rng.next_plus() >> 11) + 0.5, 0x1.0p-53);
-            const long long bx = __double_as_longlong(x);
-            const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
-            const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
-            const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-            const double t = __fma_rn(m, s_log.inv_c[ti], -1.0);
-            // log1p(t), |t| <= 2^-8, to degree 5: absolute error < 2^-50
-            double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
-            sp = __fma_rn(t, sp, 1.0 / 3.0);
-            sp = __fma_rn(t, sp, -0.5);
-            sp = __fma_rn(t, sp, 1.0);
-            const double e = static_cast<double>(ex);
-            return -__fma_rn(e, 0x1.62e42fefa39efp-1, s_log.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
-          };
-          // class of T, at or after class kf: bucket index (a lower bound) then a forward walk
-          auto class_of = [&](double T, int kf) -> int {
-            int kl = kf;
-            if (!(T < s_em[kf + 1])) {
-              const double bt = T * inv_bucket;
-              const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
-              kl = kb > kf ? kb : kf;
-              while (kl + 1 < K && !(T < s_em[kl + 1])) ++kl;
+          uint32_t pva = 0, pvb = 0, pha = 0, phb = 0;
+          double pfa = 0.0, pwa = 0.0, pfb = 0.0, pwb = 0.0;
+          uint32_t ev = 0;  // this lane's event serial (2 per round)
+          // class of T: bucket lower bound, then at most seg.depth forward
+          // steps (two branch-free compares when the table guarantees depth <= 2)
+          const bool shallow = a.seg.depth <= 2;
+          auto class_of = [&](double T) -> int {
+            const double bt = T * inv_bucket;
+            int kl = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+            if (shallow) {
+              const bool c1 = !(T < s_rec[kl + 1].em), c2 = !(T < s_rec[kl + 2].em);
+              kl += (c1 ? 1 : 0) + (c2 ? 1 : 0);
+            } else {
+              while (kl < K && !(T < s_rec[kl + 1].em)) ++kl;
             }
             return kl;
           };
-          auto position = [&](double T, int kl) -> uint32_t {
-            const uint32_t s0 = static_cast<uint32_t>(s_start[kl]);
-            const uint32_t s1 = static_cast<uint32_t>(s_start[kl + 1]);
-            uint32_t v = s0 + static_cast<uint32_t>(fmax(T - s_em[kl], 0.0) * s_iwf[kl]);
-            return v > s1 - 1 ? s1 - 1 : v;
-          };
-          // lane l takes events 2l and 2l+1 of each 64-event round
           for (;;) {
-            const bool accpa = kDefer && penda && pr2a < pwa * pfa;
-            const bool accpb = kDefer && pendb && pr2b < pwb * pfb;
+            bool accpa = false, accpb = false;
+            if (kDefer) {
+              if (penda) accpa = lazy_accept(pha, pwa * pfa, lkey, ev - 2);
+              if (pendb) accpb = lazy_accept(phb, pwb * pfb, lkey, ev - 1);
+            }
             const uint32_t pvva = pva, pvvb = pvb;
             penda = pendb = false;
-            const double Ea = exp1();
-            const double Eb = exp1();
-            const double pair = Ea + Eb;
-            const double incl = warp_incl_scan_f64(pair);
+            const uint64_t xa = rng.next(), xb = rng.next();
+            const double Ea = exp_bits(xa, s_log);
+            const double Eb = exp_bits(xb, s_log);
+            const uint32_t ha = static_cast<uint32_t>(xa) & 2047u, hb = static_cast<uint32_t>(xb) & 2047u;
+            const double incl = warp_incl_scan_f64(Ea + Eb);
             const double Ta = T0 + (incl - Eb) * inv_c;
             const double Tb = T0 + incl * inv_c;
-            // both acceptance uniforms from one xoshiro256++ draw (all 64
-            // output bits are full quality); 32-bit resolution bounds the
-            // acceptance bias by 2^-33
-            const uint64_t r2bits = rng.next();
-            const double r2a = (static_cast<double>(static_cast<uint32_t>(r2bits >> 32)) + 0.5) * 0x1.0p-32;
-            const double r2b = (static_cast<double>(static_cast<uint32_t>(r2bits)) + 0.5) * 0x1.0p-32;
-            const int kla = class_of(Ta, k);
-            const int klb = class_of(Tb, kla);
-            const uint32_t va = position(Ta, kla);
-            const uint32_t vb = position(Tb, klb);
+            const int kla = class_of(Ta);
+            const int klb = class_of(Tb);
+            const double2 eia = *reinterpret_cast<const double2*>(&s_rec[kla].em);
+            const uint2 sa = *reinterpret_cast<const uint2*>(&s_rec[kla].s0);
+            const double2 eib = *reinterpret_cast<const double2*>(&s_rec[klb].em);
+            const uint2 sb = *reinterpret_cast<const uint2*>(&s_rec[klb].s0);
+            uint32_t va = sa.x + static_cast<uint32_t>(fmax(Ta - eia.x, 0.0) * eia.y);
+            va = va > sa.y - 1 ? sa.y - 1 : va;
+            uint32_t vb = sb.x + static_cast<uint32_t>(fmax(Tb - eib.x, 0.0) * eib.y);
+            vb = vb > sb.y - 1 ? sb.y - 1 : vb;
             const bool valida = Ta < em_end && va < vend32;
             const bool validb = Tb < em_end && vb < vend32;
             uint32_t vp = __shfl_up_sync(CLG_FULL, vb, 1);
@@ -843,45 +936,68 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             const bool propa = valida && va > vp;
             const bool propb = validb && vb > va;
             const int dia = kla - kw, dib = klb - kw;
-            double ga = __shfl_sync(CLG_FULL, g_lane, dia & 31);
-            double gb = __shfl_sync(CLG_FULL, g_lane, dib & 31);
-            if (dia >= 32) ga = bern_gk(inv_kappa, c_u * s_wf[kla]);
-            if (dib >= 32) gb = bern_gk(inv_kappa, c_u * s_wf[klb]);
-            bool acca = false, accb = false;
-            if (propa) {
-              if (r2a < s_sure[kla] * ga) {
-                acca = true;
-              } else if (kDefer) {
-                penda = true;
-                pva = va;
-                pr2a = r2a;
-                pfa = ga * s_iwf[kla];
-                pwa = w[va];  // consumed next round
-              } else {
-                acca = r2a < ga * (w[va] * s_iwf[kla]);
+            uint32_t hsa = __shfl_sync(CLG_FULL, hs_lane, dia & 31);
+            uint32_t hsb = __shfl_sync(CLG_FULL, hs_lane, dib & 31);
+            const bool acca = propa && ha < hsa && dia < 32;
+            const bool accb = propb && hb < hsb && dib < 32;
+            // uncertain (or outside the window): acceptance factor f = g_k / wfirst_k
+            const bool unca = propa && !acca, uncb = propb && !accb;
+            bool acca2 = false, accb2 = false;
+            if (__any_sync(CLG_FULL, unca || uncb)) {
+              double ga = __shfl_sync(CLG_FULL, g_lane, dia & 31);
+              double gb = __shfl_sync(CLG_FULL, g_lane, dib & 31);
+              if (unca) {
+                if (dia >= 32) {
+                  ga = bern_gk(inv_kappa, c_u * s_rec[kla].wf);
+                  hsa = static_cast<uint32_t>((__ldg(g_sure + kla) * ga) * 2048.0);
+                }
+                if (ha < hsa) {
+                  acca2 = true;
+                } else {
+                  const double f = ga * eia.y;
+                  if (kDefer) {
+                    penda = true;
+                    pva = va;
+                    pha = ha;
+                    pfa = f;
+                    pwa = w[va];  // consumed next round
+                  } else {
+                    acca2 = lazy_accept(ha, w[va] * f, lkey, ev);
+                  }
+                }
+              }
+              if (uncb) {
+                if (dib >= 32) {
+                  gb = bern_gk(inv_kappa, c_u * s_rec[klb].wf);
+                  hsb = static_cast<uint32_t>((__ldg(g_sure + klb) * gb) * 2048.0);
+                }
+                if (hb < hsb) {
+                  accb2 = true;
+                } else {
+                  const double f = gb * eib.y;
+                  if (kDefer) {
+                    pendb = true;
+                    pvb = vb;
+                    phb = hb;
+                    pfb = f;
+                    pwb = w[vb];
+                  } else {
+                    accb2 = lazy_accept(hb, w[vb] * f, lkey, ev + 1);
+                  }
+                }
               }
             }
-            if (propb) {
-              if (r2b < s_sure[klb] * gb) {
-                accb = true;
-              } else if (kDefer) {
-                pendb = true;
-                pvb = vb;
-                pr2b = r2b;
-                pfb = gb * s_iwf[klb];
-                pwb = w[vb];
-              } else {
-                accb = r2b < gb * (w[vb] * s_iwf[klb]);
-              }
-            }
-            // last round's deferred accepts, then this round's
-            WARP_EMIT4(accpa, pvva, accpb, pvvb, acca, va, accb, vb)
+            ev += 2;
+            if (MODE == kWalkFold) side_push(accpa, pvva, accpb, pvvb);
+            else if (MODE == kWalkCount) emit2(accpa, pvva, accpb, pvvb);
+            emit2(acca || acca2, va, accb || accb2, vb);
             // carry the last lane's second event into the next round
             if (!__all_sync(CLG_FULL, validb)) {
               if (kDefer) {
-                const bool la = penda && pr2a < pwa * pfa;
-                const bool lb = pendb && pr2b < pwb * pfb;
-                WARP_EMIT2(la, pva, lb, pvb)
+                const bool la = penda && lazy_accept(pha, pwa * pfa, lkey, ev - 2);
+                const bool lb = pendb && lazy_accept(phb, pwb * pfb, lkey, ev - 1);
+                if (MODE == kWalkFold) side_push(la, pva, lb, pvb);
+                else emit2(la, pva, lb, pvb);
               }
               break;
             }
@@ -890,19 +1006,20 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
             prev_v = __shfl_sync(CLG_FULL, vb, 31);
             if (k - kw >= 16) {
               kw = k;
-              g_lane = kw + lane < K ? bern_gk(inv_kappa, c_u * s_wf[kw + lane]) : 0.0;
+              refresh();
             }
           }
         }
       }
     }
-#undef WARP_EMIT
-#undef WARP_EMIT2
-#undef WARP_EMIT4
-#undef EMIT_SLOT_FOLD
     if (MODE == kWalkCount && lane == 0) a.counts[unit] = cnt;
-    if (MODE == kWalkFold && lane == 0 && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
-      atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+    if (MODE == kWalkFold) {
+      side_flush();
+      if (a.degree && (u & ((1ll << a.track_shift) - 1)) == 0) {  // tracked source: its out-edges of this unit
+        const uint64_t d = warp_sum_u64(fs.edges - e_unit);
+        if (lane == 0 && d) atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(d));
+      }
+    }
   }
 
   if (a.prof.slots && lane == 0) {
@@ -910,14 +1027,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     a.prof.slots[2 * g] = t_start;
     a.prof.slots[2 * g + 1] = globaltimer_ns();
   }
-  if (MODE == kWalkFold) {
-    checksum = warp_sum_u64(checksum);
-    edges_total = warp_sum_u64(edges_total);
-    if (lane == 0) {
-      atomicAdd(&a.fold_out[0], edges_total);
-      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
-    }
-  }
+  if (MODE == kWalkFold) fs.finish(a, lane);
 }
 
 // Envelope-expected candidate count of source u over [u+1, n) (the same
@@ -1100,18 +1210,28 @@ __global__ void segment_mass_kernel(const double* __restrict__ w, Segments seg, 
   }
 }
 
-// bucket[b] = largest k with em[k] <= b * em[K] / kBuckets (a lower bound of
-// the class of any T in bucket b).
-__global__ void segment_buckets_kernel(Segments seg, unsigned short* bucket) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= kBuckets) return;
-  const double x = seg.em[seg.K] * (static_cast<double>(b) / kBuckets);
+// bucket[b] = class holding envelope mass just below b * em[K] / kBuckets (a
+// lower bound of the class of any T the lookup maps to bucket b, robust to
+// the rounding of T * kBuckets / em[K]); depth_out = max over b of the number
+// of class boundaries up to just above the bucket end.
+__device__ __forceinline__ int class_at(const Segments& seg, double x) {
   int lo = 0, hi = seg.K;  // em[lo] <= x < em[hi] (or hi = K)
   while (hi - lo > 1) {
     const int m = (lo + hi) >> 1;
     if (seg.em[m] <= x) lo = m; else hi = m;
   }
+  return lo;
+}
+
+__global__ void segment_buckets_kernel(Segments seg, unsigned short* bucket, int* depth_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= kBuckets) return;
+  const double E = seg.em[seg.K];
+  const double x0 = E * (static_cast<double>(b) / kBuckets), x1 = E * (static_cast<double>(b + 1) / kBuckets);
+  const int lo = class_at(seg, x0 - E * 0x1.0p-40);
+  const int hi = class_at(seg, x1 + E * 0x1.0p-40);
   bucket[b] = static_cast<unsigned short>(lo);
+  atomicMax(depth_out, hi - lo);
 }
 
 // First index in [lo,hi) with w < lim (hi if none); w non-increasing.  One warp.
