@@ -89,16 +89,6 @@ __device__ __forceinline__ int seg_of(const Segments& s, int64_t j) {
   return a;
 }
 
-// Same as seg_of on a (shared-memory) copy of start[].
-__device__ __forceinline__ int seg_of_s(const int64_t* start, int K, int64_t j) {
-  int a = 0, b = K;
-  while (b - a > 1) {
-    const int m = (a + b) >> 1;
-    if (start[m] <= j) a = m; else b = m;
-  }
-  return a;
-}
-
 __device__ __forceinline__ double pbar_of(double wu, double wv, double S) {
   return __ddiv_rn(__dmul_rn(wu, wv), S);  // the generators' q = w_u w_v / S
 }
@@ -118,26 +108,6 @@ __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
   return static_cast<double>(b >> 11) * 0x1.0p-53;
 }
 
-// Exp(1) by inversion, E = -log(U), U = (x>>11 + 1/2) 2^-53 in (0,1), with the
-// branch-free table log (absolute error ~2^-53: statistically exact).
-__device__ __forceinline__ double exp_inv(Xoshiro& g, const LogTable& T) {
-  const double x = __dmul_rn(static_cast<double>(g.next_plus() >> 11) + 0.5, 0x1.0p-53);
-  const long long b = __double_as_longlong(x);
-  const int E = static_cast<int>((b >> 52) & 0x7ff) - 1023;
-  const int i = static_cast<int>((b >> 45) & (kLogTable - 1));
-  const double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-  const double t = __fma_rn(m, T.inv_c[i], -1.0);
-  double s = __fma_rn(t, 1.0 / 7.0, -1.0 / 6.0);
-  s = __fma_rn(t, s, 1.0 / 5.0);
-  s = __fma_rn(t, s, -1.0 / 4.0);
-  s = __fma_rn(t, s, 1.0 / 3.0);
-  s = __fma_rn(t, s, -0.5);
-  s = __fma_rn(t, s, 1.0);
-  const double e = static_cast<double>(E);
-  // -(E ln2 + log c + log1p t)
-  return -__fma_rn(e, 0x1.62e42fefa39efp-1, T.nlog_inv[i] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * s));
-}
-
 // Key of the per-unit stream: a bijection of (u, split) mixed with the seed.
 __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint32_t split) {
   return mix64(seed_mix ^ (static_cast<uint64_t>(u) | (static_cast<uint64_t>(split) << 36)));
@@ -145,382 +115,6 @@ __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint3
 
 enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
-
-// Lane-per-unit emission of up to four edges per lane, in lane order and
-// (A0, A1, A2, A3) order within a lane; one ballot set and one ring reservation.
-#define EMIT_EDGE4(A0, V0, A1, V1, A2, V2, A3, V3) {                                                          \
-    const bool acc_[4] = {static_cast<bool>(A0), static_cast<bool>(A1), static_cast<bool>(A2), static_cast<bool>(A3)}; \
-    const int64_t vv_[4] = {static_cast<int64_t>(V0), static_cast<int64_t>(V1), static_cast<int64_t>(V2), static_cast<int64_t>(V3)}; \
-    _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                                \
-      if (acc_[e_]) {                                                                                 \
-        ++cnt;                                                                                        \
-        if (MODE == kWalkWrite) {                                                                     \
-          if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(vv_[e_])); \
-          else atomicAdd(a.overflow, 1ull);                                                           \
-          ++out_pos;                                                                                  \
-        } else if (MODE == kWalkFold) {                                                               \
-          checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(vv_[e_]));       \
-          ++edges_total;                                                                              \
-          if (a.degree && (vv_[e_] & ((1ll << a.track_shift) - 1)) == 0)                              \
-            atomicAdd(&a.degree[vv_[e_] >> a.track_shift], 1u);                                       \
-        }                                                                                             \
-      }                                                                                               \
-    }                                                                                                 \
-    if (MODE == kWalkFold && a.ring) {                                                                \
-      const unsigned b0_ = __ballot_sync(CLG_FULL, acc_[0]);                                          \
-      const unsigned b1_ = __ballot_sync(CLG_FULL, acc_[1]);                                          \
-      const unsigned b2_ = __ballot_sync(CLG_FULL, acc_[2]);                                          \
-      const unsigned b3_ = __ballot_sync(CLG_FULL, acc_[3]);                                          \
-      if (b0_ | b1_ | b2_ | b3_) {                                                                    \
-        const unsigned lt_ = lanemask_lt();                                                           \
-        const unsigned kk = __popc(b0_) + __popc(b1_) + __popc(b2_) + __popc(b3_);                    \
-        unsigned rk = __popc(b0_ & lt_) + __popc(b1_ & lt_) + __popc(b2_ & lt_) + __popc(b3_ & lt_);  \
-        const unsigned long long rem = r_end - r_next;                                                \
-        unsigned long long nb = 0;                                                                    \
-        if (rem < kk) {                                                                               \
-          if (lane == 0) nb = atomicAdd(a.ring_head, 2048ull);                                        \
-          nb = __shfl_sync(CLG_FULL, nb, 0);                                                          \
-        }                                                                                             \
-        _Pragma("unroll") for (int e_ = 0; e_ < 4; ++e_) {                                            \
-          if (acc_[e_]) {                                                                             \
-            const unsigned long long pos = rk < rem ? r_next + rk : nb + (rk - rem);                  \
-            a.ring[pos & a.ring_mask] = make_uint2(static_cast<uint32_t>(u), static_cast<uint32_t>(vv_[e_])); \
-            ++rk;                                                                                     \
-          }                                                                                           \
-        }                                                                                             \
-        if (rem < kk) {                                                                               \
-          r_next = nb + (kk - rem);                                                                   \
-          r_end = nb + 2048ull;                                                                       \
-        } else {                                                                                      \
-          r_next += kk;                                                                               \
-        }                                                                                             \
-      }                                                                                               \
-    }                                                                                                 \
-}
-
-#ifndef CLG_LANE_EVENTS
-#define CLG_LANE_EVENTS 3
-#endif
-constexpr int kLaneEvents = CLG_LANE_EVENTS;  // hazard events per lane iteration (light units)
-
-template <int MODE, int MINB>
-__global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
-                                                          const LogTable* __restrict__ logtab, uint64_t seed_mix) {
-  constexpr int64_t kBatch = 32;
-  __shared__ int64_t s_start[kSegSmemMax + 1];
-  __shared__ double s_em[kSegSmemMax + 1];
-  __shared__ double s_wf[kSegSmemMax];
-  __shared__ double s_iwf[kSegSmemMax];
-  __shared__ double s_sure[kSegSmemMax];
-  __shared__ LogTable s_log;
-  const int K = a.seg.K;  // K <= kSegSmemMax (the host widens classes otherwise)
-  for (int i = threadIdx.x; i <= K; i += blockDim.x) {
-    s_start[i] = a.seg.start[i];
-    s_em[i] = a.seg.em[i];
-    if (i < K) {
-      s_wf[i] = a.seg.wfirst[i];
-      s_iwf[i] = a.seg.invwf[i];
-      s_sure[i] = a.seg.sure[i];
-    }
-  }
-  for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
-    s_log.inv_c[i] = logtab->inv_c[i];
-    s_log.nlog_inv[i] = logtab->nlog_inv[i];
-  }
-  __shared__ unsigned short s_bucket[kBuckets];
-  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
-  __syncthreads();
-  const double inv_bucket = static_cast<double>(kBuckets) / s_em[K];
-
-  const int lane = lane_id();
-  const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
-  const double* __restrict__ w = a.w;
-  const double S = a.S;
-
-  int64_t b_next = 0, b_end = 0;
-  bool drained = false;
-  unsigned long long r_next = 0, r_end = 0;
-
-  // lane state
-  int64_t unit = -1, u = 0, j = 0, vend = 0, vsat = 0, vB = 0, seg_hi = 0, out_pos = 0;
-  int k = 0, phase = kPhHaz;
-  int32_t cnt = 0;
-  double wu = 0.0;
-  // hazard phase: proposals form a Poisson process of rate c_u * wfirst[k]
-  // per position, i.e. unit rate in T = c_u * (envelope mass); T is tracked
-  // in envelope-mass units (divided by c_u).
-  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, thr = 0.0, gk = 0.0, em_next = 0.0;
-  int64_t prev_v = 0;
-  // software-pipelined accept: an uncertain candidate's weight is loaded in
-  // one iteration and compared in the next, so the warp never waits on it
-  int64_t pend_v = -1;
-  double pend_r2 = 0.0, pend_f = 0.0, pend_w = 0.0;
-  // band phase
-  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
-  Xoshiro rng;
-  uint64_t checksum = 0;
-  unsigned long long edges_total = 0;
-
-  for (;;) {
-    const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
-    if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
-      const int want = __popc(need);
-      const int r = __popc(need & lanemask_lt());
-      const bool me = (need >> lane) & 1u;
-      int64_t mine = -1;
-      const int64_t take1 = imin64(b_end - b_next, want);
-      if (me && r < take1) mine = b_next + r;
-      b_next += take1;
-      if (want > take1) {
-        unsigned long long g = 0;
-        if (lane == 0) g = atomicAdd(a.queue, (unsigned long long)kBatch);
-        g = __shfl_sync(CLG_FULL, g, 0);
-        if (static_cast<int64_t>(g) >= a.total_units) {
-          drained = true;
-          b_next = b_end = a.total_units;
-        } else {
-          b_next = static_cast<int64_t>(g);
-          b_end = imin64(b_next + kBatch, a.total_units);
-          const int64_t take2 = imin64(b_end - b_next, want - take1);
-          if (me && r >= take1 && r - take1 < take2) mine = b_next + (r - take1);
-          b_next += take2;
-        }
-      }
-      if (mine >= 0) {
-        unit = mine;
-        uint32_t split = 0;
-        const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
-        if (mine < hub_units) {
-          int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
-          while (hi_h - lo_h > 1) {
-            const int64_t m = (lo_h + hi_h) >> 1;
-            if (a.hub_units[m] <= mine) lo_h = m; else hi_h = m;
-          }
-          u = a.lo + lo_h;
-          split = static_cast<uint32_t>(mine - a.hub_units[lo_h]);
-          j = split_pos[mine];
-          vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
-        } else {
-          u = a.lo + a.H + (mine - hub_units);
-          j = u + 1;
-          vend = a.n;
-        }
-        cnt = 0;
-        if (MODE == kWalkWrite) out_pos = a.offsets[mine];
-        wu = w[u];
-        rng.seed_key(unit_key(seed_mix, u, split));
-        if (j < vend && S > 0.0 && wu > 0.0) {
-          // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
-          const double y0 = pbar_of(wu, w[j], S);
-          if (y0 < kBandTau) {
-            vsat = vB = j;
-          } else {
-            vB = first_p_below(w, wu, S, j, vend, kBandTau);
-            vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
-          }
-          phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
-          seg_hi = 0;
-          if (vB < vend) {
-            const int kb = seg_of_s(s_start, K, vB);
-            // kappa = -log(1-ymax)/ymax from the largest envelope used
-            const double ymax = pbar_of(wu, s_wf[kb], S);
-            if (ymax > 0.0) {
-              double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
-#pragma unroll
-              for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
-              c_u = kappa * (wu / S);
-              inv_c = __drcp_rn(c_u);
-              inv_kappa = __drcp_rn(kappa);
-              T = s_em[kb] + s_wf[kb] * static_cast<double>(vB - s_start[kb]);
-              prev_v = vB - 1;
-              k = kb;
-              em_next = s_em[kb + 1];
-              // accept factor for class k: (1/kappa) * z/(1-e^-z), z = c_u wf
-              const double z = c_u * s_wf[kb], z2 = z * z;
-              gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
-                                z2 * z2 * z2 * (1.0 / 30240.0));
-              thr = s_sure[kb] * gk;
-            } else {
-              vend = vB;  // zero weights from vB on
-            }
-          }
-          if (phase == kPhBand) k = seg_of_s(s_start, K, j);
-        } else {
-          j = vend;
-        }
-      }
-    }
-    const unsigned live = __ballot_sync(CLG_FULL, unit >= 0);
-    if (!live) {
-      if (drained) break;
-      continue;
-    }
-
-    bool accepted = false, accepted1 = false, accepted2 = false;
-    int64_t v = 0, v1 = 0, v2 = 0;
-    bool finish = false;
-    // resolve the candidate whose weight was requested last iteration
-    const bool acc_prev = pend_v >= 0 && pend_r2 < pend_w * pend_f;
-    const int64_t v_prev = pend_v;
-    pend_v = -1;
-    bool pend_new = false;
-    int pend_slot = -1;
-    int64_t pv_new = 0;
-    double pr2_new = 0.0, pf_new = 0.0;
-    if (unit >= 0) {
-      if (j >= vend) {
-        finish = true;
-      } else if (phase == kPhHaz) {
-        // ---- hazard envelope: kLaneEvents events per iteration -----------
-#pragma unroll
-        for (int e = 0; e < kLaneEvents; ++e) {
-          if (finish) break;
-          bool acc_e = false;
-          int64_t v_e = 0;
-          T += exp_inv(rng, s_log) * inv_c;
-          if (!(T < em_next)) {
-            if (!(T < s_em[K])) {
-              finish = true;
-            } else {
-              const double bt = T * inv_bucket;
-              const int kb = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
-              k = kb > k + 1 ? kb : k + 1;
-              while (!(T < s_em[k + 1])) ++k;
-              em_next = s_em[k + 1];
-              const double z = c_u * s_wf[k], z2 = z * z;
-              gk = inv_kappa * (1.0 + z * 0.5 + z2 * (1.0 / 12.0) - z2 * z2 * (1.0 / 720.0) +
-                                z2 * z2 * z2 * (1.0 / 30240.0));
-              thr = s_sure[k] * gk;
-            }
-          }
-          if (!finish) {
-            const int64_t s0 = s_start[k];
-            const double iwf = s_iwf[k];
-            v_e = s0 + static_cast<int64_t>((T - s_em[k]) * iwf);
-            const int64_t s1 = s_start[k + 1];
-            if (v_e >= s1) v_e = s1 - 1;
-            if (v_e < s0) v_e = s0;
-            if (v_e >= vend) {
-              finish = true;
-            } else if (v_e > prev_v) {  // a position proposed once however many events hit it
-              prev_v = v_e;
-              const double r2 = unit53(rng.next_plus());
-              if (r2 < thr) {
-                acc_e = true;
-              } else if (!pend_new) {
-                pend_new = true;
-                pv_new = v_e;
-                pr2_new = r2;
-                pf_new = gk * iwf;
-              } else {  // second uncertain candidate of the iteration (rare): decide now
-                acc_e = r2 < w[v_e] * (gk * iwf);
-              }
-            }
-          }
-          if (e == 0) {
-            accepted = acc_e;
-            v = v_e;
-          } else if (e == 1) {
-            accepted1 = acc_e;
-            v1 = v_e;
-          } else {
-            accepted2 = acc_e;
-            v2 = v_e;
-          }
-          if (pend_new && pend_slot < 0) pend_slot = e;
-          // the write pass keeps each unit's edges in position order: an
-          // undecided event (emitted next iteration) ends this iteration
-          if (MODE == kWalkWrite && pend_new) break;
-        }
-        // the unit ends this iteration: an outstanding candidate must be
-        // decided before the lane moves on to another unit
-        if (finish && pend_new) {
-          const bool acc_p = pr2_new < w[pv_new] * pf_new;
-          if (pend_slot == 0) accepted = acc_p;
-          else if (pend_slot == 1) accepted1 = acc_p;
-          else accepted2 = acc_p;
-          pend_new = false;
-        }
-      } else if (phase == kPhSat) {
-        // ---- saturated band: q = 1, every position is an edge ------------
-        v = j;
-        accepted = true;
-        ++j;
-        if (j >= vsat) {
-          phase = vB > j ? kPhBand : kPhHaz;
-          if (phase == kPhBand) {
-            k = seg_of_s(s_start, K, j);
-            seg_hi = 0;
-          }
-        }
-      } else {
-        // ---- heavy band: exact per-class geometric skips -----------------
-        if (j >= seg_hi) {
-          while (s_start[k + 1] <= j) ++k;
-          seg_hi = imin64(s_start[k + 1], vB);
-          wf = s_wf[k];
-          pb = fmin(pbar_of(wu, wf, S), 1.0);
-          sure = s_sure[k];
-          ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
-        }
-        int64_t delta = 0;
-        bool over = false;
-        if (pb < 1.0) {
-          const double ratio = log(rng.open01()) * ilp;
-          if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
-          else delta = static_cast<int64_t>(ratio);
-        }
-        if (over) {
-          j = seg_hi;
-        } else {
-          v = j + delta;
-          const double r2 = unit53(rng.next_plus());
-          if (pb >= 1.0) {
-            const double q = pbar_of(wu, w[v], S);
-            accepted = q >= 1.0 || r2 < q;
-          } else {
-            accepted = r2 < sure || r2 * wf < w[v];
-          }
-          j = v + 1;
-        }
-        if (j >= vB) {  // hazard state (T, c_u, class factors) was prepared at unit start
-          phase = kPhHaz;
-          if (vB < vend) k = seg_of_s(s_start, K, vB);
-        }
-      }
-    }
-
-    // a new uncertain candidate: request its weight now, decide next iteration
-    // (the unit cannot finish before that: finishing draws no candidate)
-    if (pend_new) {
-      pend_v = pv_new;
-      pend_r2 = pr2_new;
-      pend_f = pf_new;
-      pend_w = w[pv_new];
-    }
-    EMIT_EDGE4(acc_prev, v_prev, accepted, v, accepted1, v1, accepted2, v2)
-    if (unit >= 0 && (finish || j >= vend)) {
-      if (MODE == kWalkCount) a.counts[unit] = cnt;
-      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
-        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
-      unit = -1;
-    }
-  }
-
-  if (a.prof.slots && lane == 0) {
-    const int g = a.prof.gw();
-    a.prof.slots[2 * g] = t_start;
-    a.prof.slots[2 * g + 1] = globaltimer_ns();
-  }
-  if (MODE == kWalkFold) {
-    checksum = warp_sum_u64(checksum);
-    edges_total = warp_sum_u64(edges_total);
-    if (lane == 0) {
-      atomicAdd(&a.fold_out[0], edges_total);
-      atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
-    }
-  }
-}
 
 // ---- warp-cooperative processing of heavy units --------------------------
 // All 32 lanes work on one unit: round r, lane l takes Poisson events 64r+2l
@@ -1022,6 +616,389 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     }
   }
 
+  if (a.prof.slots && lane == 0) {
+    const int g = a.prof.gw();
+    a.prof.slots[2 * g] = t_start;
+    a.prof.slots[2 * g + 1] = globaltimer_ns();
+  }
+  if (MODE == kWalkFold) fs.finish(a, lane);
+}
+
+// ---- light units: one lane per unit ----------------------------------------
+// Each lane walks one unit's hazard process sequentially (kLaneEvents events
+// per loop iteration); idle lanes are refilled from a warp-local batch of the
+// unit queue.  Same envelope, acceptance and lazy 11-bit acceptance bits as
+// the warp kernel; every draw comes from the unit's own stream, in event
+// order, so the count, write and fold modes make identical decisions.
+#ifndef CLG_LANE_EVENTS
+#define CLG_LANE_EVENTS 3
+#endif
+constexpr int kLaneEvents = CLG_LANE_EVENTS;  // hazard events per lane iteration (light units)
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+                                                          const LogTable* __restrict__ logtab, uint64_t seed_mix) {
+  constexpr int64_t kBatch = 32;
+  __shared__ ClassRec s_rec[kSegSmemMax + 2];
+  __shared__ LogTable s_log;
+  __shared__ unsigned short s_bucket[kBuckets];
+  __shared__ uint2 s_side[256 / 32][64];  // fold mode: deferred accepts (u, v), folded 32 at a time
+  const int K = a.seg.K;
+  for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+    ClassRec r;
+    r.em = a.seg.em[i];
+    r.iwf = i < K ? a.seg.invwf[i] : 0.0;
+    r.s0 = static_cast<uint32_t>(a.seg.start[i]);
+    r.s1 = i < K ? static_cast<uint32_t>(a.seg.start[i + 1]) : r.s0;
+    r.wf = i < K ? a.seg.wfirst[i] : 0.0;
+    s_rec[i] = r;
+    if (i == K) {
+      r.em = __longlong_as_double(0x7ff0000000000000LL);
+      r.iwf = 0.0;
+      r.wf = 0.0;
+      s_rec[K + 1] = r;
+    }
+  }
+  for (int i = threadIdx.x; i < kLogTable; i += blockDim.x) {
+    s_log.inv_c[i] = logtab->inv_c[i];
+    s_log.nlog_inv[i] = logtab->nlog_inv[i];
+  }
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
+  __syncthreads();
+  const double inv_bucket = static_cast<double>(kBuckets) / s_rec[K].em;
+  const double em_end = s_rec[K].em;
+  const bool shallow = a.seg.depth <= 2;
+  const double* __restrict__ g_sure = a.seg.sure;
+
+  const int lane = lane_id();
+  const unsigned lt_mask = lanemask_lt();
+  uint2* side = s_side[threadIdx.x >> 5];
+  unsigned side_n = 0;
+  const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
+  const double* __restrict__ w = a.w;
+  const double S = a.S;
+  const uint32_t tmask = (1u << a.track_shift) - 1u;
+  FoldSink fs;
+  fs.init(a);
+
+  int64_t b_next = 0, b_end = 0;
+  bool drained = false;
+
+  // lane state
+  int64_t unit = -1, u = 0, j = 0, vend = 0, vsat = 0, vB = 0, seg_hi = 0, out_pos = 0;
+  int k = 0, phase = kPhHaz;
+  int32_t cnt = 0;
+  double wu = 0.0;
+  uint64_t lkey = 0;
+  uint32_t ev = 0;  // event serial of the unit's hazard process
+  // hazard phase: proposals form a Poisson process of rate c_u * wfirst[k]
+  // per position, i.e. unit rate in T = c_u * (envelope mass); T is tracked
+  // in envelope-mass units (divided by c_u).
+  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, gk = 0.0, em_next = 0.0;
+  uint32_t hs = 0;  // floor(sure_k gk 2^11): R < hs/2^11 accepts without w[v]
+  uint32_t prev_v = 0, vend32 = 0;
+  // software-pipelined accept: an uncertain candidate's weight is loaded in
+  // one iteration and compared in the next, so the warp never waits on it
+  bool pend = false;
+  uint32_t pend_v = 0, pend_h = 0, pend_id = 0;
+  double pend_f = 0.0, pend_w = 0.0;
+  // band phase
+  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
+  Xoshiro rng;
+
+  auto set_class = [&](int kn) {
+    k = kn;
+    em_next = s_rec[kn + 1].em;
+    gk = bern_gk(inv_kappa, c_u * s_rec[kn].wf);
+    hs = kn < K ? static_cast<uint32_t>((__ldg(g_sure + kn) * gk) * 2048.0) : 0u;
+  };
+  auto class_of = [&](double t) -> int {
+    const double bt = t * inv_bucket;
+    int kl = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+    if (shallow) {
+      const bool c1 = !(t < s_rec[kl + 1].em), c2 = !(t < s_rec[kl + 2].em);
+      kl += (c1 ? 1 : 0) + (c2 ? 1 : 0);
+    } else {
+      while (kl < K && !(t < s_rec[kl + 1].em)) ++kl;
+    }
+    return kl;
+  };
+  // fold mode: stage the deferred accept of this iteration; fold 32 at a time
+  auto side_push = [&](bool c, uint32_t uu, uint32_t vv) {
+    const unsigned b = __ballot_sync(CLG_FULL, c);
+    if (b == 0u) return;
+    if (c) side[side_n + __popc(b & lt_mask)] = make_uint2(uu, vv);
+    side_n += __popc(b);
+    if (side_n >= 32) {
+      __syncwarp();
+      const uint2 e = side[lane], en = side[32 + lane];
+      __syncwarp();
+      side[lane] = en;
+      fs.emit2(a, e.x, tmask, lt_mask, lane, true, e.y, false, 0u);
+      side_n -= 32;
+    }
+  };
+
+  for (;;) {
+    const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
+    if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
+      const int want = __popc(need);
+      const int r = __popc(need & lt_mask);
+      const bool me = (need >> lane) & 1u;
+      int64_t mine = -1;
+      const int64_t take1 = imin64(b_end - b_next, want);
+      if (me && r < take1) mine = b_next + r;
+      b_next += take1;
+      if (want > take1) {
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(a.queue, (unsigned long long)kBatch);
+        g = __shfl_sync(CLG_FULL, g, 0);
+        if (static_cast<int64_t>(g) >= a.total_units) {
+          drained = true;
+          b_next = b_end = a.total_units;
+        } else {
+          b_next = static_cast<int64_t>(g);
+          b_end = imin64(b_next + kBatch, a.total_units);
+          const int64_t take2 = imin64(b_end - b_next, want - take1);
+          if (me && r >= take1 && r - take1 < take2) mine = b_next + (r - take1);
+          b_next += take2;
+        }
+      }
+      if (mine >= 0) {
+        unit = mine;
+        uint32_t split = 0;
+        const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
+        if (mine < hub_units) {
+          int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
+          while (hi_h - lo_h > 1) {
+            const int64_t m = (lo_h + hi_h) >> 1;
+            if (a.hub_units[m] <= mine) lo_h = m; else hi_h = m;
+          }
+          u = a.lo + lo_h;
+          split = static_cast<uint32_t>(mine - a.hub_units[lo_h]);
+          j = split_pos[mine];
+          vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
+        } else {
+          u = a.lo + a.H + (mine - hub_units);
+          j = u + 1;
+          vend = a.n;
+        }
+        cnt = 0;
+        ev = 0;
+        if (MODE == kWalkWrite) out_pos = a.offsets[mine];
+        wu = w[u];
+        lkey = unit_key(seed_mix, u, split);
+        rng.seed_key(lkey);
+        vend32 = static_cast<uint32_t>(vend);
+        if (j < vend && S > 0.0 && wu > 0.0) {
+          // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
+          const double y0 = pbar_of(wu, w[j], S);
+          if (y0 < kBandTau) {
+            vsat = vB = j;
+          } else {
+            vB = first_p_below(w, wu, S, j, vend, kBandTau);
+            vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
+          }
+          phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
+          seg_hi = 0;
+          if (vB < vend) {
+            const int kb = rec_of(s_rec, K, vB);
+            // kappa = -log(1-ymax)/ymax from the largest envelope used
+            const double ymax = pbar_of(wu, s_rec[kb].wf, S);
+            if (ymax > 0.0) {
+              double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
+#pragma unroll
+              for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
+              c_u = kappa * (wu / S);
+              inv_c = __drcp_rn(c_u);
+              inv_kappa = __drcp_rn(kappa);
+              T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[kb].s0));
+              prev_v = static_cast<uint32_t>(vB - 1);
+              set_class(kb);
+            } else {
+              vend = vB;  // zero weights from vB on
+              vend32 = static_cast<uint32_t>(vend);
+            }
+          }
+          if (phase == kPhBand) k = rec_of(s_rec, K, j);
+        } else {
+          j = vend;
+        }
+      }
+    }
+    const unsigned live = __ballot_sync(CLG_FULL, unit >= 0);
+    if (!live) {
+      if (drained) break;
+      continue;
+    }
+
+    bool acc[kLaneEvents];
+    uint32_t vv[kLaneEvents];
+#pragma unroll
+    for (int e = 0; e < kLaneEvents; ++e) {
+      acc[e] = false;
+      vv[e] = 0;
+    }
+    bool finish = false;
+    // resolve the candidate whose weight was requested last iteration
+    const bool acc_prev = pend && lazy_accept(pend_h, pend_w * pend_f, lkey, pend_id);
+    const uint32_t v_prev = pend_v;
+    pend = false;
+    bool pend_new = false;
+    int pend_slot = -1;
+    uint32_t pv_new = 0, ph_new = 0, pid_new = 0;
+    double pf_new = 0.0;
+    if (unit >= 0) {
+      if (j >= vend) {
+        finish = true;
+      } else if (phase == kPhHaz) {
+        // ---- hazard envelope: kLaneEvents events per iteration -----------
+#pragma unroll
+        for (int e = 0; e < kLaneEvents; ++e) {
+          if (finish) break;
+          const uint64_t x = rng.next();
+          T += exp_bits(x, s_log) * inv_c;
+          const uint32_t h = static_cast<uint32_t>(x) & 2047u;
+          const uint32_t id = ev++;
+          if (!(T < em_next)) {
+            if (!(T < em_end)) finish = true;
+            else set_class(class_of(T));
+          }
+          if (!finish) {
+            const ClassRec& rc = s_rec[k];
+            uint32_t v_e = rc.s0 + static_cast<uint32_t>(fmax(T - rc.em, 0.0) * rc.iwf);
+            v_e = v_e > rc.s1 - 1 ? rc.s1 - 1 : v_e;
+            if (v_e >= vend32) {
+              finish = true;
+            } else if (v_e > prev_v) {  // a position proposed once however many events hit it
+              prev_v = v_e;
+              vv[e] = v_e;
+              if (h < hs) {
+                acc[e] = true;
+              } else if (!pend_new) {
+                pend_new = true;
+                pend_slot = e;
+                pv_new = v_e;
+                ph_new = h;
+                pid_new = id;
+                pf_new = gk * rc.iwf;
+              } else {  // second uncertain candidate of the iteration (rare): decide now
+                acc[e] = lazy_accept(h, w[v_e] * (gk * rc.iwf), lkey, id);
+              }
+            }
+          }
+          // the write pass keeps each unit's edges in position order: an
+          // undecided event (emitted next iteration) ends this iteration
+          if (MODE == kWalkWrite && pend_new) break;
+        }
+        // the unit ends this iteration: an outstanding candidate must be
+        // decided before the lane moves on to another unit
+        if (finish && pend_new) {
+          const bool acc_p = lazy_accept(ph_new, w[pv_new] * pf_new, lkey, pid_new);
+#pragma unroll
+          for (int e = 0; e < kLaneEvents; ++e)
+            if (e == pend_slot) acc[e] = acc_p;
+          pend_new = false;
+        }
+      } else if (phase == kPhSat) {
+        // ---- saturated band: q = 1, every position is an edge ------------
+        vv[0] = static_cast<uint32_t>(j);
+        acc[0] = true;
+        ++j;
+        if (j >= vsat) {
+          phase = vB > j ? kPhBand : kPhHaz;
+          if (phase == kPhBand) {
+            k = rec_of(s_rec, K, j);
+            seg_hi = 0;
+          }
+        }
+      } else {
+        // ---- heavy band: exact per-class geometric skips -----------------
+        if (j >= seg_hi) {
+          while (static_cast<int64_t>(s_rec[k + 1].s0) <= j) ++k;
+          seg_hi = imin64(static_cast<int64_t>(s_rec[k + 1].s0), vB);
+          wf = s_rec[k].wf;
+          pb = fmin(pbar_of(wu, wf, S), 1.0);
+          sure = __ldg(g_sure + k);
+          ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
+        }
+        int64_t delta = 0;
+        bool over = false;
+        if (pb < 1.0) {
+          const double ratio = log(rng.open01()) * ilp;
+          if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
+          else delta = static_cast<int64_t>(ratio);
+        }
+        if (over) {
+          j = seg_hi;
+        } else {
+          const int64_t v = j + delta;
+          const double r2 = unit53(rng.next_plus());
+          vv[0] = static_cast<uint32_t>(v);
+          if (pb >= 1.0) {
+            const double q = pbar_of(wu, w[v], S);
+            acc[0] = q >= 1.0 || r2 < q;
+          } else {
+            acc[0] = r2 < sure || r2 * wf < w[v];
+          }
+          j = v + 1;
+        }
+        if (j >= vB) {  // hazard state (T, c_u, class factors) was prepared at unit start
+          phase = kPhHaz;
+          if (vB < vend) set_class(rec_of(s_rec, K, vB));
+        }
+      }
+    }
+
+    // a new uncertain candidate: request its weight now, decide next iteration
+    // (the unit cannot finish before that: finishing draws no candidate)
+    if (pend_new) {
+      pend = true;
+      pend_v = pv_new;
+      pend_h = ph_new;
+      pend_id = pid_new;
+      pend_f = pf_new;
+      pend_w = w[pv_new];
+    }
+    // emission: the previous iteration's deferred accept, then this iteration's
+    cnt += (acc_prev ? 1 : 0);
+#pragma unroll
+    for (int e = 0; e < kLaneEvents; ++e) cnt += acc[e] ? 1 : 0;
+    const uint32_t u32 = static_cast<uint32_t>(u);
+    if (MODE == kWalkWrite) {
+      if (acc_prev) {
+        if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(u32, v_prev); else atomicAdd(a.overflow, 1ull);
+        ++out_pos;
+      }
+#pragma unroll
+      for (int e = 0; e < kLaneEvents; ++e) {
+        if (acc[e]) {
+          if (out_pos < a.cap) a.pairs[out_pos] = make_uint2(u32, vv[e]); else atomicAdd(a.overflow, 1ull);
+          ++out_pos;
+        }
+      }
+    } else if (MODE == kWalkFold) {
+      side_push(acc_prev, u32, v_prev);
+#pragma unroll
+      for (int e = 0; e + 1 < kLaneEvents; e += 2)
+        fs.emit2(a, u32, tmask, lt_mask, lane, acc[e], vv[e], acc[e + 1], vv[e + 1]);
+      if (kLaneEvents & 1)
+        fs.emit2(a, u32, tmask, lt_mask, lane, acc[kLaneEvents - 1], vv[kLaneEvents - 1], false, 0u);
+    }
+    if (unit >= 0 && (finish || j >= vend)) {
+      if (MODE == kWalkCount) a.counts[unit] = cnt;
+      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+      unit = -1;
+    }
+  }
+
+  if (MODE == kWalkFold && side_n > 0) {  // < 32 staged accepts left
+    __syncwarp();
+    const bool c = static_cast<unsigned>(lane) < side_n;
+    const uint2 e = side[lane];
+    fs.emit2(a, e.x, tmask, lt_mask, lane, c, e.y, false, 0u);
+  }
   if (a.prof.slots && lane == 0) {
     const int g = a.prof.gw();
     a.prof.slots[2 * g] = t_start;
