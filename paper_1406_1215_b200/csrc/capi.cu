@@ -135,6 +135,7 @@ struct clgen_dev_ctx {
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   int seg_depth = 64;  // bucket lookup depth (segment_buckets_kernel)
+  int seg_nb = clg::kBuckets;  // buckets in the class index
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
@@ -143,6 +144,7 @@ struct clgen_dev_ctx {
   DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
+  size_t ctr_warp_smem[3] = {0, 0, 0};
   // optional per-warp busy intervals of the sampler kernels
   bool warp_prof = false;
   DevBuf prof;
@@ -449,14 +451,21 @@ int ensure_segments(clgen_dev_ctx* c) {
       sg.K = K;
       clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
       clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>());
-      CUDA_TRY(cudaMemsetAsync(&c->sc->total, 0, sizeof(int64_t), c->stream));
-      clg::segment_buckets_kernel<<<clg::kBuckets / 256, 256, 0, c->stream>>>(
-          sg, c->seg_bucket.as<unsigned short>(), reinterpret_cast<int*>(&c->sc->total));
-      c->launches += 3;
-      CUDA_TRY(cudaGetLastError());
+      // smallest bucket index (4096, then 8192) whose lookups need <= 2 steps
       int depth = 0;
-      CUDA_TRY(cudaMemcpyAsync(&depth, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      for (int nb = 4096; nb <= clg::kBuckets; nb *= 2) {
+        sg.nb = nb;
+        CUDA_TRY(cudaMemsetAsync(&c->sc->total, 0, sizeof(int64_t), c->stream));
+        clg::segment_buckets_kernel<<<(nb + 255) / 256, 256, 0, c->stream>>>(
+            sg, c->seg_bucket.as<unsigned short>(), reinterpret_cast<int*>(&c->sc->total));
+        ++c->launches;
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(&depth, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        c->seg_nb = nb;
+        if (depth <= 2) break;
+      }
+      c->launches += 2;
       c->seg_depth = depth;
       c->seg_valid = true;
       return CLGEN_OK;
@@ -468,7 +477,7 @@ int ensure_segments(clgen_dev_ctx* c) {
 clg::Segments segments(clgen_dev_ctx* c) {
   return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
                        c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
-                       c->seg_bucket.as<unsigned short>(), c->seg_depth};
+                       c->seg_bucket.as<unsigned short>(), c->seg_depth, c->seg_nb};
 }
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected
@@ -611,31 +620,44 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
                            c->stream));
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   if (c->ctr_heavy > 0) {
-    static const int wminb = [] {
-      const char* e = std::getenv("CLGEN_WARP_MINB");
-      const int v = e ? std::atoi(e) : 3;
-      return v >= 2 && v <= 4 ? v : 3;
+    // block shape of the warp kernel: CLGEN_WARP_CFG = 256x3 (default) | 256x2 | 256x4 | 128x6 | 128x7 | 128x8
+    static const int wcfg = [] {
+      const char* e = std::getenv("CLGEN_WARP_CFG");
+      const std::string v = e ? e : "";
+      if (v == "256x2") return 0;
+      if (v == "256x4") return 2;
+      if (v == "128x6") return 3;
+      if (v == "128x7") return 4;
+      if (v == "128x8") return 5;
+      return 1;
     }();
-    if (!c->ctr_warp_blocks[MODE]) {
-      int per_sm = 0;
-      if (wminb == 2) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 2>, 256, 0));
-      else if (wminb == 4) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 4>, 256, 0));
-      else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_warp_kernel<MODE, 3>, 256, 0));
-      c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    const int threads = wcfg >= 3 ? 128 : 256;
+    const size_t smem = clg::ctr_warp_smem_bytes(c->seg_K, c->seg_nb, threads);
+    auto launch = [&](auto kern) -> int {
+      if (!c->ctr_warp_blocks[MODE] || c->ctr_warp_smem[MODE] != smem) {
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+        c->ctr_warp_smem[MODE] = smem;
+      }
+      const int g = c->ctr_warp_blocks[MODE];
+      a.prof = prof_slots(c, g * threads / 256, true);
+      kern<<<g, threads, smem, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix, c->ctr_heavy,
+                                             &c->sc->queue_heavy);
+      CUDA_TRY(cudaGetLastError());
+      ++c->launches;
+      return CLGEN_OK;
+    };
+    int rc;
+    switch (wcfg) {
+      case 0: rc = launch(clg::ctr_warp_kernel<MODE, 256, 2>); break;
+      case 2: rc = launch(clg::ctr_warp_kernel<MODE, 256, 4>); break;
+      case 3: rc = launch(clg::ctr_warp_kernel<MODE, 128, 6>); break;
+      case 4: rc = launch(clg::ctr_warp_kernel<MODE, 128, 7>); break;
+      case 5: rc = launch(clg::ctr_warp_kernel<MODE, 128, 8>); break;
+      default: rc = launch(clg::ctr_warp_kernel<MODE, 256, 3>); break;
     }
-    const int g = c->ctr_warp_blocks[MODE];
-    a.prof = prof_slots(c, g, true);
-    if (wminb == 2)
-      clg::ctr_warp_kernel<MODE, 2><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
-                                                               c->ctr_heavy, &c->sc->queue_heavy);
-    else if (wminb == 4)
-      clg::ctr_warp_kernel<MODE, 4><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
-                                                               c->ctr_heavy, &c->sc->queue_heavy);
-    else
-      clg::ctr_warp_kernel<MODE, 3><<<g, 256, 0, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix,
-                                                               c->ctr_heavy, &c->sc->queue_heavy);
-    CUDA_TRY(cudaGetLastError());
-    ++c->launches;
+    if (rc) return rc;
   }
   if (c->ctr_units > c->ctr_heavy) {
     int rc;

@@ -45,9 +45,10 @@ struct Segments {
   const unsigned short* bucket;  // kBuckets entries: a lower bound of the class of any T in bucket b
   int depth;  // max over buckets of (classes a bucket can reach) - 1: the class of T is within
               // [bucket[b], bucket[b] + depth]
+  int nb;     // number of buckets (<= kBuckets)
 };
 
-constexpr int kBuckets = 8192;
+constexpr int kBuckets = 8192;  // bucket table capacity
 
 constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA (static smem < 48 KB)
 constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
@@ -176,7 +177,7 @@ __device__ __forceinline__ bool lazy_accept(uint32_t h, double a, uint64_t key, 
 // slots assigned lane-major by one ballot pair.
 struct FoldSink {
   uint64_t checksum;
-  unsigned long long edges;
+  uint32_t edges;   // per lane (< 2^32 over a launch)
   uint2* seg;       // this warp's ring segment (nullptr: no ring)
   uint32_t smask;   // segment length - 1
   uint32_t wpos;    // edges this warp has written (warp-uniform)
@@ -220,7 +221,7 @@ struct FoldSink {
   // warp totals into fold_out[0..1]
   __device__ __forceinline__ void finish(const CtrWalkArgs& a, int lane) {
     const uint64_t c = warp_sum_u64(checksum);
-    const uint64_t e = warp_sum_u64(edges);
+    const uint64_t e = warp_sum_u64(static_cast<uint64_t>(edges));
     if (lane == 0) {
       atomicAdd(&a.fold_out[0], static_cast<unsigned long long>(e));
       atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(c));
@@ -250,15 +251,26 @@ __device__ __forceinline__ int rec_of(const ClassRec* r, int K, int64_t j) {
   return a;
 }
 
-template <int MODE, int MINB>
-__global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
-                                                          const LogTable* __restrict__ logtab, uint64_t seed_mix,
-                                                          int64_t U_heavy, unsigned long long* queue_heavy) {
-  __shared__ ClassRec s_rec[kSegSmemMax + 2];
-  __shared__ LogTable s_log;
-  __shared__ unsigned short s_bucket[kBuckets];
-  __shared__ uint32_t s_side[256 / 32][kSideCap];
+// Dynamic shared memory of the warp kernel: K+2 class records, the log
+// table, the bucket index and the per-warp staging of deferred accepts.
+__host__ __device__ inline size_t ctr_warp_smem_bytes(int K, int nb, int threads) {
+  return static_cast<size_t>(K + 2) * sizeof(ClassRec) + sizeof(LogTable) +
+         ((static_cast<size_t>(nb) * sizeof(unsigned short) + 15) & ~size_t(15)) +
+         static_cast<size_t>(threads / 32) * kSideCap * sizeof(uint32_t);
+}
+
+template <int MODE, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
+                                                              const LogTable* __restrict__ logtab, uint64_t seed_mix,
+                                                              int64_t U_heavy, unsigned long long* queue_heavy) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.seg.K;
+  const int NB = a.seg.nb;
+  ClassRec* s_rec = reinterpret_cast<ClassRec*>(smem_raw);
+  LogTable& s_log = *reinterpret_cast<LogTable*>(smem_raw + static_cast<size_t>(K + 2) * sizeof(ClassRec));
+  unsigned short* s_bucket = reinterpret_cast<unsigned short*>(reinterpret_cast<unsigned char*>(&s_log) + sizeof(LogTable));
+  uint32_t* s_side = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_bucket) +
+                                                 ((static_cast<size_t>(NB) * sizeof(unsigned short) + 15) & ~size_t(15)));
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
     ClassRec r;
     r.em = a.seg.em[i];
@@ -278,13 +290,13 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     s_log.inv_c[i] = logtab->inv_c[i];
     s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
-  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
-  const double inv_bucket = static_cast<double>(kBuckets) / s_rec[K].em;
+  const double inv_bucket = static_cast<double>(NB) / s_rec[K].em;
   const double* __restrict__ g_sure = a.seg.sure;
 
   const int lane = lane_id();
-  uint32_t* side = s_side[threadIdx.x >> 5];
+  uint32_t* side = s_side + (threadIdx.x >> 5) * kSideCap;
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const unsigned lt_mask = lanemask_lt();
   const double* __restrict__ w = a.w;
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
         side_n = 0;
       }
     };
-    const unsigned long long e_unit = fs.edges;
+    const uint32_t e_unit = fs.edges;
 
     if (j < vend && S > 0.0 && wu > 0.0) {
       const double y0 = pbar_of(wu, w[j], S);
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
           const bool shallow = a.seg.depth <= 2;
           auto class_of = [&](double T) -> int {
             const double bt = T * inv_bucket;
-            int kl = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+            int kl = s_bucket[bt < static_cast<double>(NB - 1) ? static_cast<int>(bt) : NB - 1];
             if (shallow) {
               const bool c1 = !(T < s_rec[kl + 1].em), c2 = !(T < s_rec[kl + 2].em);
               kl += (c1 ? 1 : 0) + (c2 ? 1 : 0);
@@ -610,7 +622,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_warp_kernel(CtrWalkArgs a, cons
     if (MODE == kWalkFold) {
       side_flush();
       if (a.degree && (u & ((1ll << a.track_shift) - 1)) == 0) {  // tracked source: its out-edges of this unit
-        const uint64_t d = warp_sum_u64(fs.edges - e_unit);
+        const uint64_t d = warp_sum_u64(static_cast<uint64_t>(fs.edges - e_unit));
         if (lane == 0 && d) atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(d));
       }
     }
@@ -663,9 +675,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     s_log.inv_c[i] = logtab->inv_c[i];
     s_log.nlog_inv[i] = logtab->nlog_inv[i];
   }
-  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
+  const int NB = a.seg.nb;
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
-  const double inv_bucket = static_cast<double>(kBuckets) / s_rec[K].em;
+  const double inv_bucket = static_cast<double>(NB) / s_rec[K].em;
   const double em_end = s_rec[K].em;
   const bool shallow = a.seg.depth <= 2;
   const double* __restrict__ g_sure = a.seg.sure;
@@ -714,7 +727,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   };
   auto class_of = [&](double t) -> int {
     const double bt = t * inv_bucket;
-    int kl = s_bucket[bt < static_cast<double>(kBuckets - 1) ? static_cast<int>(bt) : kBuckets - 1];
+    int kl = s_bucket[bt < static_cast<double>(NB - 1) ? static_cast<int>(bt) : NB - 1];
     if (shallow) {
       const bool c1 = !(t < s_rec[kl + 1].em), c2 = !(t < s_rec[kl + 2].em);
       kl += (c1 ? 1 : 0) + (c2 ? 1 : 0);
@@ -1202,9 +1215,9 @@ __device__ __forceinline__ int class_at(const Segments& seg, double x) {
 
 __global__ void segment_buckets_kernel(Segments seg, unsigned short* bucket, int* depth_out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= kBuckets) return;
+  if (b >= seg.nb) return;
   const double E = seg.em[seg.K];
-  const double x0 = E * (static_cast<double>(b) / kBuckets), x1 = E * (static_cast<double>(b + 1) / kBuckets);
+  const double x0 = E * (static_cast<double>(b) / seg.nb), x1 = E * (static_cast<double>(b + 1) / seg.nb);
   const int lo = class_at(seg, x0 - E * 0x1.0p-40);
   const int hi = class_at(seg, x1 + E * 0x1.0p-40);
   bucket[b] = static_cast<unsigned short>(lo);
