@@ -136,6 +136,7 @@ struct clgen_dev_ctx {
   int seg_K = 0;
   int seg_depth = 64;  // bucket lookup depth (segment_buckets_kernel)
   int seg_nb = clg::kBuckets;  // buckets in the class index
+  double seg_em_end = 0.0;     // envelope mass em[K]
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
@@ -467,6 +468,7 @@ int ensure_segments(clgen_dev_ctx* c) {
       }
       c->launches += 2;
       c->seg_depth = depth;
+      CUDA_TRY(cudaMemcpy(&c->seg_em_end, c->seg_em.as<double>() + K, sizeof(double), cudaMemcpyDeviceToHost));
       c->seg_valid = true;
       return CLGEN_OK;
     }
@@ -477,7 +479,8 @@ int ensure_segments(clgen_dev_ctx* c) {
 clg::Segments segments(clgen_dev_ctx* c) {
   return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
                        c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
-                       c->seg_bucket.as<unsigned short>(), c->seg_depth, c->seg_nb};
+                       c->seg_bucket.as<unsigned short>(), c->seg_depth, c->seg_nb, c->seg_em_end,
+                       static_cast<double>(c->seg_nb) / c->seg_em_end};
 }
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected
@@ -620,16 +623,17 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
                            c->stream));
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   if (c->ctr_heavy > 0) {
-    // block shape of the warp kernel: CLGEN_WARP_CFG = 256x3 (default) | 256x2 | 256x4 | 128x6 | 128x7 | 128x8
+    // block shape of the warp kernel: CLGEN_WARP_CFG = 256x4 (default: 64 registers, 32 warps/SM) |
+    // 256x2 | 256x3 | 128x6 | 128x7 | 128x8
     static const int wcfg = [] {
       const char* e = std::getenv("CLGEN_WARP_CFG");
       const std::string v = e ? e : "";
       if (v == "256x2") return 0;
-      if (v == "256x4") return 2;
+      if (v == "256x3") return 1;
       if (v == "128x6") return 3;
       if (v == "128x7") return 4;
       if (v == "128x8") return 5;
-      return 1;
+      return 2;
     }();
     const int threads = wcfg >= 3 ? 128 : 256;
     const size_t smem = clg::ctr_warp_smem_bytes(c->seg_K, c->seg_nb, threads);
@@ -651,11 +655,11 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
     int rc;
     switch (wcfg) {
       case 0: rc = launch(clg::ctr_warp_kernel<MODE, 256, 2>); break;
-      case 2: rc = launch(clg::ctr_warp_kernel<MODE, 256, 4>); break;
+      case 1: rc = launch(clg::ctr_warp_kernel<MODE, 256, 3>); break;
       case 3: rc = launch(clg::ctr_warp_kernel<MODE, 128, 6>); break;
       case 4: rc = launch(clg::ctr_warp_kernel<MODE, 128, 7>); break;
       case 5: rc = launch(clg::ctr_warp_kernel<MODE, 128, 8>); break;
-      default: rc = launch(clg::ctr_warp_kernel<MODE, 256, 3>); break;
+      default: rc = launch(clg::ctr_warp_kernel<MODE, 256, 4>); break;
     }
     if (rc) return rc;
   }

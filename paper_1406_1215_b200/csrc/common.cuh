@@ -79,6 +79,39 @@ struct Xoshiro {
   }
 };
 
+// xoroshiro128++ (Blackman & Vigna): the counter stream's per-(unit, lane)
+// generator.  128-bit state seeded by two splitmix64 outputs of the stream
+// key; all 64 output bits are full quality (the samplers use the top 53 for
+// an exponential and the low 11 as acceptance bits).
+struct Xoro128 {
+  uint64_t s0, s1;
+
+  __device__ __forceinline__ void seed_key(uint64_t key) {
+    s0 = mix64(key);
+    s1 = mix64(key + 0x9e3779b97f4a7c15ULL);
+    if ((s0 | s1) == 0) s0 = 1;
+  }
+
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t a = s0;
+    uint64_t b = s1;
+    const uint64_t result = rotl64(a + b, 17) + a;
+    b ^= a;
+    s0 = rotl64(a, 49) ^ b ^ (b << 21);
+    s1 = rotl64(b, 28);
+    return result;
+  }
+
+  __device__ __forceinline__ uint64_t next_plus() { return next(); }
+
+  __device__ __forceinline__ double open01() {
+    for (;;) {
+      const double r = __dmul_rn(static_cast<double>(next() >> 11), 0x1.0p-53);
+      if (r > 0.0) return r;
+    }
+  }
+};
+
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 

@@ -46,6 +46,8 @@ struct Segments {
   int depth;  // max over buckets of (classes a bucket can reach) - 1: the class of T is within
               // [bucket[b], bucket[b] + depth]
   int nb;     // number of buckets (<= kBuckets)
+  double em_end;      // em[K]
+  double inv_bucket;  // nb / em[K]
 };
 
 constexpr int kBuckets = 8192;  // bucket table capacity
@@ -292,7 +294,6 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
   }
   for (int i = threadIdx.x; i < NB; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
-  const double inv_bucket = static_cast<double>(NB) / s_rec[K].em;
   const double* __restrict__ g_sure = a.seg.sure;
 
   const int lane = lane_id();
@@ -301,11 +302,10 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
   const unsigned lt_mask = lanemask_lt();
   const double* __restrict__ w = a.w;
   const double S = a.S;
-  const double em_end = s_rec[K].em;
   const uint32_t tmask = (1u << a.track_shift) - 1u;
   FoldSink fs;
   fs.init(a);
-  Xoshiro rng;
+  Xoro128 rng;
 
   for (;;) {
     unsigned long long ug = 0;
@@ -492,15 +492,16 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
           // count/fold modes resolve an uncertain accept one round later (its
           // w[v] load overlaps the next round); the ordered write pass cannot
           constexpr bool kDefer = MODE != kWalkWrite;
-          bool penda = false, pendb = false;
-          uint32_t pva = 0, pvb = 0, pha = 0, phb = 0;
-          double pfa = 0.0, pwa = 0.0, pfb = 0.0, pwb = 0.0;
+          // one deferred candidate per lane: (position, acceptance bits | event b flag << 16, factor, weight)
+          bool pend = false;
+          uint32_t pv = 0, ph = 0;
+          double pf = 0.0, pw = 0.0;
           uint32_t ev = 0;  // this lane's event serial (2 per round)
           // class of T: bucket lower bound, then at most seg.depth forward
           // steps (two branch-free compares when the table guarantees depth <= 2)
           const bool shallow = a.seg.depth <= 2;
           auto class_of = [&](double T) -> int {
-            const double bt = T * inv_bucket;
+            const double bt = T * a.seg.inv_bucket;
             int kl = s_bucket[bt < static_cast<double>(NB - 1) ? static_cast<int>(bt) : NB - 1];
             if (shallow) {
               const bool c1 = !(T < s_rec[kl + 1].em), c2 = !(T < s_rec[kl + 2].em);
@@ -511,13 +512,9 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
             return kl;
           };
           for (;;) {
-            bool accpa = false, accpb = false;
-            if (kDefer) {
-              if (penda) accpa = lazy_accept(pha, pwa * pfa, lkey, ev - 2);
-              if (pendb) accpb = lazy_accept(phb, pwb * pfb, lkey, ev - 1);
-            }
-            const uint32_t pvva = pva, pvvb = pvb;
-            penda = pendb = false;
+            const bool accp = kDefer && pend && lazy_accept(ph & 0xffffu, pw * pf, lkey, ev - 2 + (ph >> 16));
+            const uint32_t pvv = pv;
+            pend = false;
             const uint64_t xa = rng.next(), xb = rng.next();
             const double Ea = exp_bits(xa, s_log);
             const double Eb = exp_bits(xb, s_log);
@@ -535,8 +532,8 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
             va = va > sa.y - 1 ? sa.y - 1 : va;
             uint32_t vb = sb.x + static_cast<uint32_t>(fmax(Tb - eib.x, 0.0) * eib.y);
             vb = vb > sb.y - 1 ? sb.y - 1 : vb;
-            const bool valida = Ta < em_end && va < vend32;
-            const bool validb = Tb < em_end && vb < vend32;
+            const bool valida = Ta < a.seg.em_end && va < vend32;
+            const bool validb = Tb < a.seg.em_end && vb < vend32;
             uint32_t vp = __shfl_up_sync(CLG_FULL, vb, 1);
             if (lane == 0) vp = prev_v;
             const bool propa = valida && va > vp;
@@ -562,11 +559,11 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
                 } else {
                   const double f = ga * eia.y;
                   if (kDefer) {
-                    penda = true;
-                    pva = va;
-                    pha = ha;
-                    pfa = f;
-                    pwa = w[va];  // consumed next round
+                    pend = true;
+                    pv = va;
+                    ph = ha;
+                    pf = f;
+                    pw = w[va];  // consumed next round
                   } else {
                     acca2 = lazy_accept(ha, w[va] * f, lkey, ev);
                   }
@@ -581,29 +578,28 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
                   accb2 = true;
                 } else {
                   const double f = gb * eib.y;
-                  if (kDefer) {
-                    pendb = true;
-                    pvb = vb;
-                    phb = hb;
-                    pfb = f;
-                    pwb = w[vb];
-                  } else {
+                  if (kDefer && !pend) {
+                    pend = true;
+                    pv = vb;
+                    ph = hb | (1u << 16);
+                    pf = f;
+                    pw = w[vb];
+                  } else {  // write mode, or a second uncertain event this round (rare): decide now
                     accb2 = lazy_accept(hb, w[vb] * f, lkey, ev + 1);
                   }
                 }
               }
             }
             ev += 2;
-            if (MODE == kWalkFold) side_push(accpa, pvva, accpb, pvvb);
-            else if (MODE == kWalkCount) emit2(accpa, pvva, accpb, pvvb);
+            if (MODE == kWalkFold) side_push(accp, pvv, false, 0u);
+            else if (MODE == kWalkCount) emit2(accp, pvv, false, 0u);
             emit2(acca || acca2, va, accb || accb2, vb);
             // carry the last lane's second event into the next round
             if (!__all_sync(CLG_FULL, validb)) {
               if (kDefer) {
-                const bool la = penda && lazy_accept(pha, pwa * pfa, lkey, ev - 2);
-                const bool lb = pendb && lazy_accept(phb, pwb * pfb, lkey, ev - 1);
-                if (MODE == kWalkFold) side_push(la, pva, lb, pvb);
-                else emit2(la, pva, lb, pvb);
+                const bool lp = pend && lazy_accept(ph & 0xffffu, pw * pf, lkey, ev - 2 + (ph >> 16));
+                if (MODE == kWalkFold) side_push(lp, pv, false, 0u);
+                else emit2(lp, pv, false, 0u);
               }
               break;
             }
@@ -717,7 +713,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   double pend_f = 0.0, pend_w = 0.0;
   // band phase
   double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
-  Xoshiro rng;
+  Xoro128 rng;
 
   auto set_class = [&](int kn) {
     k = kn;

@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_counter.py tests/test_gpu_fullsize.py -q -x > gpurun_out/t3.log 2>&1; echo rc=$? >> gpurun_out/t3.log
-bash tools/ab.sh "--config c4 --num-vertices 200000000 --steps 3 --warmup 3" build/lib_v6.so build/lib_v6.so:CLGEN_WARP_CFG=128x7 build/lib_v6.so:CLGEN_WARP_CFG=128x8
+bash tools/ab.sh "--config c4 --num-vertices 200000000 --steps 3 --warmup 3" build/lib_v7.so build/lib_v7.so:CLGEN_WARP_CFG=256x4 build/lib_v7.so:CLGEN_WARP_CFG=128x7
