@@ -168,7 +168,7 @@ __device__ __forceinline__ bool lazy_accept(uint32_t h, double a, uint64_t key, 
   const double s = a * 2048.0;  // exact scaling
   if (static_cast<double>(h + 1u) <= s) return true;
   if (static_cast<double>(h) >= s) return false;
-  const uint64_t r = mix64(key + 0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(id) + 1ull));
+  const uint64_t r = mix64((key ^ 0xd6e8feb86659fd93ULL) + 0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(id) + 1ull));
   return unit53(r) < s - static_cast<double>(h);  // s - h exact (Sterbenz)
 }
 
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
     int64_t out_pos = MODE == kWalkWrite ? a.offsets[unit] : 0;
     int32_t cnt = 0;
     // lane streams: key(u, split) mixed with the lane
-    const uint64_t lkey = mix64(unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1));
+    const uint64_t lkey = unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1);
     rng.seed_key(lkey);
 
     // emission of up to two edges per lane, lane-major (c0 before c1)
