@@ -122,6 +122,14 @@ int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
  * per-warp busy time, mean and max in ms, the span first-start to last-end,
  * and the number of warps. */
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
+
+/* Counter-stream kernel shape (no reference counterpart; the edge set does
+ * not depend on it): warp_cfg selects the heavy-unit kernel's block shape
+ * (0 = 256 threads x 2 blocks/SM, 1 = 256x3, 2 = 256x4 (default), 3 = 128x6,
+ * 4 = 128x7, 5 = 128x8, -1 = CLGEN_WARP_CFG or the default); deep_lookup != 0
+ * forces the forward-walk class lookup instead of the two-compare bucket
+ * lookup.  Used by the schedule-invariance tests. */
+int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int warp_cfg, int deep_lookup);
 int clgen_dev_warp_profile_launches(clgen_dev_ctx* ctx);
 int clgen_dev_warp_profile(clgen_dev_ctx* ctx, int launch, double* max_over_mean, double* mean_ms,
                            double* max_ms, double* span_ms, int64_t* warps);

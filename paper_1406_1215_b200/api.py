@@ -145,6 +145,11 @@ class Device:
         reference expressions everywhere; both give identical edges."""
         check(_lib.lib().clgen_dev_set_fast_math(self._h, int(bool(enable))))
 
+    def set_kernel_shape(self, warp_cfg: int = -1, deep_lookup: bool = False) -> None:
+        """Counter-stream kernel shape (block shape of the heavy-unit kernel,
+        forward-walk class lookup); the edge set does not depend on it."""
+        check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(warp_cfg), int(bool(deep_lookup))))
+
     def set_warp_profile(self, enable: bool = True) -> None:
         check(_lib.lib().clgen_dev_set_warp_profile(self._h, int(bool(enable))))
 

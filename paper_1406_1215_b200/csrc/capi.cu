@@ -146,6 +146,9 @@ struct clgen_dev_ctx {
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
   size_t ctr_warp_smem[3] = {0, 0, 0};
+  int ctr_warp_cfg[3] = {-1, -1, -1};
+  int warp_cfg = -1;       // clgen_dev_set_kernel_shape (-1: CLGEN_WARP_CFG / default)
+  bool force_deep = false;  // class lookup by forward walk (test hook)
   // optional per-warp busy intervals of the sampler kernels
   bool warp_prof = false;
   DevBuf prof;
@@ -479,7 +482,7 @@ int ensure_segments(clgen_dev_ctx* c) {
 clg::Segments segments(clgen_dev_ctx* c) {
   return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
                        c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
-                       c->seg_bucket.as<unsigned short>(), c->seg_depth, c->seg_nb, c->seg_em_end,
+                       c->seg_bucket.as<unsigned short>(), c->force_deep ? 64 : c->seg_depth, c->seg_nb, c->seg_em_end,
                        static_cast<double>(c->seg_nb) / c->seg_em_end};
 }
 
@@ -576,6 +579,7 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   a.w = c->w;
   a.n = c->n;
   a.S = S;
+  a.invS = 1.0 / S;
   a.lo = lo;
   a.hi = hi;
   c->seed_mix = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
@@ -625,7 +629,7 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
   if (c->ctr_heavy > 0) {
     // block shape of the warp kernel: CLGEN_WARP_CFG = 256x4 (default: 64 registers, 32 warps/SM) |
     // 256x2 | 256x3 | 128x6 | 128x7 | 128x8
-    static const int wcfg = [] {
+    static const int wcfg_env = [] {
       const char* e = std::getenv("CLGEN_WARP_CFG");
       const std::string v = e ? e : "";
       if (v == "256x2") return 0;
@@ -635,14 +639,16 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
       if (v == "128x8") return 5;
       return 2;
     }();
+    const int wcfg = c->warp_cfg >= 0 ? c->warp_cfg : wcfg_env;
     const int threads = wcfg >= 3 ? 128 : 256;
     const size_t smem = clg::ctr_warp_smem_bytes(c->seg_K, c->seg_nb, threads);
     auto launch = [&](auto kern) -> int {
-      if (!c->ctr_warp_blocks[MODE] || c->ctr_warp_smem[MODE] != smem) {
+      if (!c->ctr_warp_blocks[MODE] || c->ctr_warp_smem[MODE] != smem || c->ctr_warp_cfg[MODE] != wcfg) {
         int per_sm = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
         c->ctr_warp_smem[MODE] = smem;
+        c->ctr_warp_cfg[MODE] = wcfg;
       }
       const int g = c->ctr_warp_blocks[MODE];
       a.prof = prof_slots(c, g * threads / 256, true);
@@ -1301,6 +1307,14 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double spli
 }
 
 int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* c) { return c ? c->ctr_heavy : -1; }
+
+int clgen_dev_set_kernel_shape(clgen_dev_ctx* c, int warp_cfg, int deep_lookup) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (warp_cfg < -1 || warp_cfg > 5) return fail(CLGEN_EINVAL, "set_kernel_shape: warp_cfg must be in [-1, 5]");
+  c->warp_cfg = warp_cfg;
+  c->force_deep = deep_lookup != 0;
+  return CLGEN_OK;
+}
 
 int clgen_dev_set_warp_profile(clgen_dev_ctx* c, int enable) {
   if (!c) return fail(CLGEN_EINVAL, "null context");

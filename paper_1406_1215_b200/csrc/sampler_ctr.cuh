@@ -59,6 +59,7 @@ struct CtrWalkArgs {
   const double* __restrict__ w;
   int64_t n;
   double S;
+  double invS;             // 1 / S (screens and envelope rates only; pbar itself is w_u w_v / S)
   int64_t lo, hi;          // source range [lo,hi)
   Segments seg;
   // hub splitting: sources [lo, lo+H) are split; unit prefix over them
@@ -393,11 +394,15 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
     const uint32_t e_unit = fs.edges;
 
     if (j < vend && S > 0.0 && wu > 0.0) {
-      const double y0 = pbar_of(wu, w[j], S);
       int64_t vB = j, vsat = j;
-      if (y0 >= kBandTau) {
-        vB = first_p_below(w, wu, S, j, vend, kBandTau);
-        vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
+      // bands only where the first pair is near or above pbar = 1/16 (the
+      // multiply-only screen leaves a 0.1% margin to the exact test)
+      if (!(wu * w[j] * a.invS < kBandTau * 0.999)) {
+        const double y0 = pbar_of(wu, w[j], S);
+        if (y0 >= kBandTau) {
+          vB = first_p_below(w, wu, S, j, vend, kBandTau);
+          vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
+        }
       }
       // ---- saturated band: every position is an edge (cooperative) ----
       for (int64_t p0 = j; p0 < vsat; p0 += 32) {
@@ -457,14 +462,14 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
       // Node ids are < 2^32 here (n <= 2^32 - 1, checked by set_weights).
       if (vB < vend) {
         int k = rec_of(s_rec, K, vB);
-        const double ymax = pbar_of(wu, s_rec[k].wf, S);
+        const double ymax = wu * s_rec[k].wf * a.invS;  // any kappa >= -log(1-ymax)/ymax keeps the law
         if (ymax > 0.0) {
           // kappa = -log(1-y)/y = sum_k y^k/(k+1) (y < (1+eps)/16: 16 terms
           // leave < 1e-19); reciprocals by one rcp each
           double kappa = 1.0 / 17.0;
 #pragma unroll
           for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
-          const double c_u = kappa * (wu / S);
+          const double c_u = kappa * (wu * a.invS);
           const double inv_c = __drcp_rn(c_u);
           const double inv_kappa = __drcp_rn(kappa);
           double T0 = s_rec[k].em + s_rec[k].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[k].s0));
@@ -801,7 +806,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         vend32 = static_cast<uint32_t>(vend);
         if (j < vend && S > 0.0 && wu > 0.0) {
           // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
-          const double y0 = pbar_of(wu, w[j], S);
+          const double y0 = wu * w[j] * a.invS < kBandTau * 0.999 ? 0.0 : pbar_of(wu, w[j], S);
           if (y0 < kBandTau) {
             vsat = vB = j;
           } else {
@@ -813,12 +818,12 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           if (vB < vend) {
             const int kb = rec_of(s_rec, K, vB);
             // kappa = -log(1-ymax)/ymax from the largest envelope used
-            const double ymax = pbar_of(wu, s_rec[kb].wf, S);
+            const double ymax = wu * s_rec[kb].wf * a.invS;
             if (ymax > 0.0) {
               double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
 #pragma unroll
               for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
-              c_u = kappa * (wu / S);
+              c_u = kappa * (wu * a.invS);
               inv_c = __drcp_rn(c_u);
               inv_kappa = __drcp_rn(kappa);
               T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[kb].s0));

@@ -137,3 +137,26 @@ def test_heavy_light_split_and_law(api, port):
     tot = sum(api.stream_range(ws, ws.sum_S, int(b[g]), int(b[g + 1]), 99, mode="counter").count
               for g in range(4))
     assert tot == full.count
+
+
+@pytest.mark.parametrize("name,n", [("c3", 2_000_000), ("c4", 4_000_000), ("c5", 1_000_000)])
+def test_kernel_shape_invariance(api, name, n):
+    """The counter-stream graph is a function of (weights, seed) only: every
+    block shape of the heavy-unit kernel (2-4 resident 256-thread blocks,
+    128-thread blocks) and the forward-walk class lookup give the same edge
+    count, checksum and tracked degrees, and the materialised pass matches."""
+    from paper_1406_1215_b200 import workloads
+    w = workloads.make(name, n)
+    ws = api.make_weight_sequence(w)
+    base = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
+    assert ws.device.counter_plan_info()["heavy_units"] > 0
+    for cfg, deep in ((0, False), (1, False), (2, True), (3, False), (4, False), (5, True)):
+        ws.device.set_kernel_shape(cfg, deep)
+        r = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
+        assert (r.count, r.checksum) == (base.count, base.checksum), (cfg, deep)
+        np.testing.assert_array_equal(r.degree, base.degree)
+    ws.device.set_kernel_shape(-1, True)
+    e = api.generate_range(ws, ws.sum_S, 0, n, 31)
+    assert len(e) == base.count and stats.checksum(e) == base.checksum
+    canon_ok(e, n)
+    ws.device.set_kernel_shape(-1, False)
