@@ -656,7 +656,9 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   __shared__ LogTable s_log;
   __shared__ unsigned short s_bucket[kBuckets];
   __shared__ uint2 s_side[256 / 32][64];  // fold mode: deferred accepts (u, v), folded 32 at a time
+  __shared__ float s_suref[kSegSmemMax];   // sure_k rounded down to float
   const int K = a.seg.K;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) s_suref[i] = __double2float_rd(a.seg.sure[i]);
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
     ClassRec r;
     r.em = a.seg.em[i];
@@ -708,8 +710,10 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   // hazard phase: proposals form a Poisson process of rate c_u * wfirst[k]
   // per position, i.e. unit rate in T = c_u * (envelope mass); T is tracked
   // in envelope-mass units (divided by c_u).
-  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, gk = 0.0, em_next = 0.0;
-  uint32_t hs = 0;  // floor(sure_k gk 2^11): R < hs/2^11 accepts without w[v]
+  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, hsc = 0.0, em_next = 0.0;
+  // hs = floor(sure_k (2^11 / kappa) (1 - 2^-40)) <= floor(sure_k g_k 2^11)
+  // (g_k >= 1/kappa): R < hs/2^11 accepts without w[v] and without g_k
+  uint32_t hs = 0;
   uint32_t prev_v = 0, vend32 = 0;
   // software-pipelined accept: an uncertain candidate's weight is loaded in
   // one iteration and compared in the next, so the warp never waits on it
@@ -723,8 +727,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   auto set_class = [&](int kn) {
     k = kn;
     em_next = s_rec[kn + 1].em;
-    gk = bern_gk(inv_kappa, c_u * s_rec[kn].wf);
-    hs = kn < K ? static_cast<uint32_t>((__ldg(g_sure + kn) * gk) * 2048.0) : 0u;
+    hs = kn < K ? static_cast<uint32_t>(static_cast<double>(s_suref[kn]) * hsc) : 0u;
   };
   auto class_of = [&](double t) -> int {
     const double bt = t * inv_bucket;
@@ -826,6 +829,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
               c_u = kappa * (wu * a.invS);
               inv_c = __drcp_rn(c_u);
               inv_kappa = __drcp_rn(kappa);
+              hsc = (2048.0 * inv_kappa) * (1.0 - 0x1.0p-40);
               T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[kb].s0));
               prev_v = static_cast<uint32_t>(vB - 1);
               set_class(kb);
@@ -889,15 +893,18 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
               vv[e] = v_e;
               if (h < hs) {
                 acc[e] = true;
-              } else if (!pend_new) {
-                pend_new = true;
-                pend_slot = e;
-                pv_new = v_e;
-                ph_new = h;
-                pid_new = id;
-                pf_new = gk * rc.iwf;
-              } else {  // second uncertain candidate of the iteration (rare): decide now
-                acc[e] = lazy_accept(h, w[v_e] * (gk * rc.iwf), lkey, id);
+              } else {
+                const double fk = bern_gk(inv_kappa, c_u * rc.wf) * rc.iwf;  // g_k / wfirst_k
+                if (!pend_new) {
+                  pend_new = true;
+                  pend_slot = e;
+                  pv_new = v_e;
+                  ph_new = h;
+                  pid_new = id;
+                  pf_new = fk;
+                } else {  // second uncertain candidate of the iteration (rare): decide now
+                  acc[e] = lazy_accept(h, w[v_e] * fk, lkey, id);
+                }
               }
             }
           }
