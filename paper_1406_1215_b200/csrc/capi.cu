@@ -303,7 +303,7 @@ int blocked_sum_impl(clgen_dev_ctx* c, const double* d, int64_t n, double* S) {
   const unsigned grid = static_cast<unsigned>((nblocks + 127) / 128);
   clg::blocked_partials_kernel<<<grid, 128, 0, c->stream>>>(d, n, c->partials.as<double>(), nblocks);
   CUDA_TRY(cudaGetLastError());
-  clg::fold_partials_kernel<<<1, 32, 0, c->stream>>>(c->partials.as<double>(), nblocks, &c->sc->S);
+  clg::fold_partials_kernel<<<1, 256, 0, c->stream>>>(c->partials.as<double>(), nblocks, &c->sc->S);
   CUDA_TRY(cudaGetLastError());
   c->launches += 2;
   if ((rc = fetch_scalars(c))) return rc;

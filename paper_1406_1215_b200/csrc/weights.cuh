@@ -34,13 +34,33 @@ __global__ void __launch_bounds__(128) blocked_partials_kernel(const double* __r
   if (blk0 + t < nblocks) part[blk0 + t] = acc;
 }
 
-// weights.cpp:27: partials combined left to right from 0.0.
-__global__ void fold_partials_kernel(const double* __restrict__ part, int64_t nblocks,
-                                     double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// weights.cpp:27: partials combined left to right from 0.0.  One block:
+// the threads stage chunks of partials in shared memory (double-buffered)
+// while thread 0 folds the previous chunk in order, so the sequential fold
+// waits on shared-memory loads, not on DRAM.
+constexpr int kFoldChunk = 2048;
+__global__ void __launch_bounds__(256) fold_partials_kernel(const double* __restrict__ part, int64_t nblocks,
+                                                            double* __restrict__ out) {
+  __shared__ double buf[2][kFoldChunk];
   double total = 0.0;
-  for (int64_t i = 0; i < nblocks; ++i) total = __dadd_rn(total, part[i]);
-  *out = total;
+  const int64_t nchunks = (nblocks + kFoldChunk - 1) / kFoldChunk;
+  for (int i = threadIdx.x; i < kFoldChunk; i += blockDim.x)
+    if (i < nblocks) buf[0][i] = part[i];
+  __syncthreads();
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int cur = static_cast<int>(c & 1);
+    const int64_t base = c * kFoldChunk;
+    if (threadIdx.x == 0) {
+      const int m = static_cast<int>(nblocks - base < kFoldChunk ? nblocks - base : kFoldChunk);
+      for (int i = 0; i < m; ++i) total = __dadd_rn(total, buf[cur][i]);
+    } else if (c + 1 < nchunks) {
+      const int64_t nb = base + kFoldChunk;
+      for (int i = threadIdx.x - 1; i < kFoldChunk; i += blockDim.x - 1)
+        if (nb + i < nblocks) buf[cur ^ 1][i] = part[nb + i];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = total;
 }
 
 // First position u with w[u] > w[u-1] (or NaN/negative), else n; `runs`
