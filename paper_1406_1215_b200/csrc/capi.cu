@@ -216,6 +216,10 @@ int reset_scalars(clgen_dev_ctx* c, unsigned long long queue_start) {
 int fetch_scalars(clgen_dev_ctx* c) {
   CUDA_TRY(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  // the light-unit kernel flags units the plan should have sent to the warp kernel
+  if (c->sc_host->overflow >= (1ull << 40))
+    return fail(CLGEN_EINVAL, "counter stream: internal plan violation (%llu light units with a band)",
+                static_cast<unsigned long long>(c->sc_host->overflow >> 40));
   return CLGEN_OK;
 }
 
@@ -566,7 +570,16 @@ int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
         hi_b = nb;
       }
     }
-    c->ctr_heavy = hub_total + (lo_b - a0);
+    // light units must be plain pure-hazard sources (no pbar >= 1/16 band):
+    // the band screen is monotone in u, so those form a suffix
+    clg::first_pure_hazard_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, a0, hi, 1.0 / S,
+                                                           reinterpret_cast<long long*>(&c->sc->total));
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    long long pure0 = hi;
+    CUDA_TRY(cudaMemcpyAsync(&pure0, &c->sc->total, sizeof pure0, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->ctr_heavy = hub_total + (std::max<int64_t>(lo_b, pure0) - a0);
   }
   c->ctr_lo = lo;
   c->ctr_hi = hi;

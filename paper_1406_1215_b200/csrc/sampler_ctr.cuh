@@ -681,10 +681,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   const int NB = a.seg.nb;
   for (int i = threadIdx.x; i < NB; i += blockDim.x) s_bucket[i] = a.seg.bucket[i];
   __syncthreads();
-  const double inv_bucket = static_cast<double>(NB) / s_rec[K].em;
-  const double em_end = s_rec[K].em;
   const bool shallow = a.seg.depth <= 2;
-  const double* __restrict__ g_sure = a.seg.sure;
 
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
@@ -700,28 +697,28 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   int64_t b_next = 0, b_end = 0;
   bool drained = false;
 
-  // lane state
-  int64_t unit = -1, u = 0, j = 0, vend = 0, vsat = 0, vB = 0, seg_hi = 0, out_pos = 0;
-  int k = 0, phase = kPhHaz;
+  // lane state (light units are plain sources whose hazard envelope starts
+  // at u+1: the host routes hubs and sources with a pbar >= 1/16 band to the
+  // warp kernel)
+  int64_t unit = -1, u = 0, out_pos = 0;
+  int k = 0;
   int32_t cnt = 0;
-  double wu = 0.0;
   uint64_t lkey = 0;
   uint32_t ev = 0;  // event serial of the unit's hazard process
-  // hazard phase: proposals form a Poisson process of rate c_u * wfirst[k]
-  // per position, i.e. unit rate in T = c_u * (envelope mass); T is tracked
-  // in envelope-mass units (divided by c_u).
+  // proposals form a Poisson process of rate c_u * wfirst[k] per position,
+  // i.e. unit rate in T = c_u * (envelope mass); T is tracked in
+  // envelope-mass units (divided by c_u).
   double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, hsc = 0.0, em_next = 0.0;
   // hs = floor(sure_k (2^11 / kappa) (1 - 2^-40)) <= floor(sure_k g_k 2^11)
   // (g_k >= 1/kappa): R < hs/2^11 accepts without w[v] and without g_k
   uint32_t hs = 0;
-  uint32_t prev_v = 0, vend32 = 0;
+  uint32_t prev_v = 0;
+  bool done = true;  // the lane's unit has no events left
   // software-pipelined accept: an uncertain candidate's weight is loaded in
   // one iteration and compared in the next, so the warp never waits on it
   bool pend = false;
   uint32_t pend_v = 0, pend_h = 0, pend_id = 0;
   double pend_f = 0.0, pend_w = 0.0;
-  // band phase
-  double wf = 0.0, ilp = 0.0, sure = 0.0, pb = 0.0;
   Xoro128 rng;
 
   auto set_class = [&](int kn) {
@@ -730,7 +727,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     hs = kn < K ? static_cast<uint32_t>(static_cast<double>(s_suref[kn]) * hsc) : 0u;
   };
   auto class_of = [&](double t) -> int {
-    const double bt = t * inv_bucket;
+    const double bt = t * a.seg.inv_bucket;
     int kl = s_bucket[bt < static_cast<double>(NB - 1) ? static_cast<int>(bt) : NB - 1];
     if (shallow) {
       const bool c1 = !(t < s_rec[kl + 1].em), c2 = !(t < s_rec[kl + 2].em);
@@ -755,6 +752,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       side_n -= 32;
     }
   };
+  const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
 
   for (;;) {
     const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
@@ -783,64 +781,34 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       }
       if (mine >= 0) {
         unit = mine;
-        uint32_t split = 0;
-        const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
-        if (mine < hub_units) {
-          int64_t lo_h = 0, hi_h = a.H;  // hub_units[lo_h] <= mine < hub_units[hi_h]
-          while (hi_h - lo_h > 1) {
-            const int64_t m = (lo_h + hi_h) >> 1;
-            if (a.hub_units[m] <= mine) lo_h = m; else hi_h = m;
-          }
-          u = a.lo + lo_h;
-          split = static_cast<uint32_t>(mine - a.hub_units[lo_h]);
-          j = split_pos[mine];
-          vend = mine + 1 == a.hub_units[lo_h + 1] ? a.n : split_pos[mine + 1];
-        } else {
-          u = a.lo + a.H + (mine - hub_units);
-          j = u + 1;
-          vend = a.n;
-        }
+        u = a.lo + a.H + (mine - hub_units);
         cnt = 0;
         ev = 0;
+        done = true;
         if (MODE == kWalkWrite) out_pos = a.offsets[mine];
-        wu = w[u];
-        lkey = unit_key(seed_mix, u, split);
+        const double wu = w[u];
+        lkey = unit_key(seed_mix, u, 0);
         rng.seed_key(lkey);
-        vend32 = static_cast<uint32_t>(vend);
-        if (j < vend && S > 0.0 && wu > 0.0) {
-          // bands: [j, vsat) saturated, [vsat, vB) pbar in [1/16, 1), [vB, vend) hazard envelope
-          const double y0 = wu * w[j] * a.invS < kBandTau * 0.999 ? 0.0 : pbar_of(wu, w[j], S);
-          if (y0 < kBandTau) {
-            vsat = vB = j;
-          } else {
-            vB = first_p_below(w, wu, S, j, vend, kBandTau);
-            vsat = y0 >= 1.0 ? first_p_below(w, wu, S, j, vB, 1.0) : j;
-          }
-          phase = vsat > j ? kPhSat : (vB > j ? kPhBand : kPhHaz);
-          seg_hi = 0;
-          if (vB < vend) {
-            const int kb = rec_of(s_rec, K, vB);
-            // kappa = -log(1-ymax)/ymax from the largest envelope used
-            const double ymax = wu * s_rec[kb].wf * a.invS;
-            if (ymax > 0.0) {
-              double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
+        const int64_t j = u + 1;
+        if (mine < hub_units || (j < a.n && !(wu * w[j] * a.invS < kBandTau * 0.999))) {
+          atomicAdd(a.overflow, 1ull << 40);  // plan violation: not a light unit (reported as an error)
+        } else if (j < a.n && S > 0.0 && wu > 0.0) {
+          const int kb = rec_of(s_rec, K, j);
+          // kappa = -log(1-ymax)/ymax from the largest envelope used
+          const double ymax = wu * s_rec[kb].wf * a.invS;
+          if (ymax > 0.0) {
+            double kappa = 1.0 / 17.0;  // -log(1-y)/y, 16 series terms (y < 1/8)
 #pragma unroll
-              for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
-              c_u = kappa * (wu * a.invS);
-              inv_c = __drcp_rn(c_u);
-              inv_kappa = __drcp_rn(kappa);
-              hsc = (2048.0 * inv_kappa) * (1.0 - 0x1.0p-40);
-              T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[kb].s0));
-              prev_v = static_cast<uint32_t>(vB - 1);
-              set_class(kb);
-            } else {
-              vend = vB;  // zero weights from vB on
-              vend32 = static_cast<uint32_t>(vend);
-            }
+            for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
+            c_u = kappa * (wu * a.invS);
+            inv_c = __drcp_rn(c_u);
+            inv_kappa = __drcp_rn(kappa);
+            hsc = (2048.0 * inv_kappa) * (1.0 - 0x1.0p-40);
+            T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(j - static_cast<int64_t>(s_rec[kb].s0));
+            prev_v = static_cast<uint32_t>(u);
+            set_class(kb);
+            done = false;
           }
-          if (phase == kPhBand) k = rec_of(s_rec, K, j);
-        } else {
-          j = vend;
         }
       }
     }
@@ -867,9 +835,9 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     uint32_t pv_new = 0, ph_new = 0, pid_new = 0;
     double pf_new = 0.0;
     if (unit >= 0) {
-      if (j >= vend) {
+      if (done) {
         finish = true;
-      } else if (phase == kPhHaz) {
+      } else {
         // ---- hazard envelope: kLaneEvents events per iteration -----------
 #pragma unroll
         for (int e = 0; e < kLaneEvents; ++e) {
@@ -879,16 +847,14 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           const uint32_t h = static_cast<uint32_t>(x) & 2047u;
           const uint32_t id = ev++;
           if (!(T < em_next)) {
-            if (!(T < em_end)) finish = true;
+            if (!(T < a.seg.em_end)) finish = true;
             else set_class(class_of(T));
           }
           if (!finish) {
             const ClassRec& rc = s_rec[k];
             uint32_t v_e = rc.s0 + static_cast<uint32_t>(fmax(T - rc.em, 0.0) * rc.iwf);
             v_e = v_e > rc.s1 - 1 ? rc.s1 - 1 : v_e;
-            if (v_e >= vend32) {
-              finish = true;
-            } else if (v_e > prev_v) {  // a position proposed once however many events hit it
+            if (v_e > prev_v) {  // a position proposed once however many events hit it
               prev_v = v_e;
               vv[e] = v_e;
               if (h < hs) {
@@ -920,53 +886,6 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           for (int e = 0; e < kLaneEvents; ++e)
             if (e == pend_slot) acc[e] = acc_p;
           pend_new = false;
-        }
-      } else if (phase == kPhSat) {
-        // ---- saturated band: q = 1, every position is an edge ------------
-        vv[0] = static_cast<uint32_t>(j);
-        acc[0] = true;
-        ++j;
-        if (j >= vsat) {
-          phase = vB > j ? kPhBand : kPhHaz;
-          if (phase == kPhBand) {
-            k = rec_of(s_rec, K, j);
-            seg_hi = 0;
-          }
-        }
-      } else {
-        // ---- heavy band: exact per-class geometric skips -----------------
-        if (j >= seg_hi) {
-          while (static_cast<int64_t>(s_rec[k + 1].s0) <= j) ++k;
-          seg_hi = imin64(static_cast<int64_t>(s_rec[k + 1].s0), vB);
-          wf = s_rec[k].wf;
-          pb = fmin(pbar_of(wu, wf, S), 1.0);
-          sure = __ldg(g_sure + k);
-          ilp = pb < 1.0 ? 1.0 / log1p(-pb) : 0.0;
-        }
-        int64_t delta = 0;
-        bool over = false;
-        if (pb < 1.0) {
-          const double ratio = log(rng.open01()) * ilp;
-          if (!(ratio < static_cast<double>(seg_hi - j))) over = true;
-          else delta = static_cast<int64_t>(ratio);
-        }
-        if (over) {
-          j = seg_hi;
-        } else {
-          const int64_t v = j + delta;
-          const double r2 = unit53(rng.next_plus());
-          vv[0] = static_cast<uint32_t>(v);
-          if (pb >= 1.0) {
-            const double q = pbar_of(wu, w[v], S);
-            acc[0] = q >= 1.0 || r2 < q;
-          } else {
-            acc[0] = r2 < sure || r2 * wf < w[v];
-          }
-          j = v + 1;
-        }
-        if (j >= vB) {  // hazard state (T, c_u, class factors) was prepared at unit start
-          phase = kPhHaz;
-          if (vB < vend) set_class(rec_of(s_rec, K, vB));
         }
       }
     }
@@ -1006,7 +925,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       if (kLaneEvents & 1)
         fs.emit2(a, u32, tmask, lt_mask, lane, acc[kLaneEvents - 1], vv[kLaneEvents - 1], false, 0u);
     }
-    if (unit >= 0 && (finish || j >= vend)) {
+    if (unit >= 0 && finish) {
       if (MODE == kWalkCount) a.counts[unit] = cnt;
       if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
         atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
@@ -1230,6 +1149,34 @@ __global__ void segment_buckets_kernel(Segments seg, unsigned short* bucket, int
   const int hi = class_at(seg, x1 + E * 0x1.0p-40);
   bucket[b] = static_cast<unsigned short>(lo);
   atomicMax(depth_out, hi - lo);
+}
+
+// First source u in [lo,hi) whose hazard envelope starts at u+1, i.e. that
+// passes the light kernel's band screen (u+1 >= n or w[u] w[u+1] / S below
+// 1/16 with the 0.1% margin); hi if none.  The predicate is monotone in u
+// (w non-increasing).  One warp.
+__global__ void first_pure_hazard_kernel(const double* __restrict__ w, int64_t n, int64_t lo0, int64_t hi0,
+                                         double invS, long long* out) {
+  const int lane = threadIdx.x;
+  auto pure = [&](int64_t u) { return u + 1 >= n || w[u] * w[u + 1] * invS < kBandTau * 0.999; };
+  int64_t lo = lo0 - 1, hi = hi0;  // answer in (lo, hi]
+  while (hi - lo > 1) {
+    const int64_t span = hi - lo - 1;
+    const int64_t step = (span + 31) / 32;
+    const int64_t p = lo + 1 + static_cast<int64_t>(lane) * step;
+    const bool ok = p >= hi || pure(p);
+    const unsigned m = __ballot_sync(CLG_FULL, ok);
+    if (m == 0) {
+      lo = lo + 1 + 31 * step;
+      continue;
+    }
+    const int f = __ffs(m) - 1;
+    const int64_t pf = lo + 1 + static_cast<int64_t>(f) * step;
+    const int64_t nlo = f > 0 ? lo + 1 + static_cast<int64_t>(f - 1) * step : lo;
+    hi = pf < hi ? pf : hi;
+    lo = nlo;
+  }
+  if (lane == 0) *out = hi;
 }
 
 // First index in [lo,hi) with w < lim (hi if none); w non-increasing.  One warp.
