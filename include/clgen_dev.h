@@ -107,8 +107,8 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
                              int64_t* n_flagged);
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
- * w_last inside a class; default 1/32) and the hub split size in expected
- * candidates (default 4096).  Changing them changes the generated graph. */
+ * w_last inside a class; default 1/64) and the hub split size in expected
+ * candidates (default 8192).  Changing them changes the generated graph. */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);
 /* Reference stream arithmetic: 1 (default) = fast guarded FP64 (table log,
  * series log1p, FMA-certified divisions; falls back to the reference

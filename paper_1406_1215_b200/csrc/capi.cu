@@ -139,9 +139,9 @@ struct clgen_dev_ctx {
   double seg_em_end = 0.0;     // envelope mass em[K]
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
-  double split_cap = env_double("CLGEN_CTR_SPLIT", 4096.0);
+  double split_cap = env_double("CLGEN_CTR_SPLIT", 8192.0);
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
-  double heavy_cand = env_double("CLGEN_CTR_HEAVY", 128.0);  // units with >= this many expected candidates run warp-cooperatively
+  double heavy_cand = env_double("CLGEN_CTR_HEAVY", 384.0);  // units with >= this many expected candidates run warp-cooperatively
   DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
