@@ -457,8 +457,8 @@ int ensure_segments(clgen_dev_ctx* c) {
       c->seg_K = K;
       clg::Segments sg = segments(c);
       sg.K = K;
-      clg::segment_mass_kernel<<<K, 256, 0, c->stream>>>(c->w, sg, c->seg_mass.as<double>());
-      clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>());
+      clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>(),
+                                                            c->seg_mass.as<double>());
       // smallest bucket index (4096, then 8192) whose lookups need <= 2 steps
       int depth = 0;
       for (int nb = 4096; nb <= clg::kBuckets; nb *= 2) {
@@ -473,7 +473,7 @@ int ensure_segments(clgen_dev_ctx* c) {
         c->seg_nb = nb;
         if (depth <= 2) break;
       }
-      c->launches += 2;
+      ++c->launches;  // segment_envelope_kernel
       c->seg_depth = depth;
       CUDA_TRY(cudaMemcpy(&c->seg_em_end, c->seg_em.as<double>() + K, sizeof(double), cudaMemcpyDeviceToHost));
       c->seg_valid = true;

@@ -1095,36 +1095,22 @@ __global__ void hub_positions_kernel(const double* __restrict__ w, int64_t n, do
   }
 }
 
-// Envelope-mass prefix em[k] and 1/wfirst (one thread; K is small).
-__global__ void segment_envelope_kernel(Segments seg, double* em, double* invwf) {
+// Envelope-mass prefix em[k], 1/wfirst and the per-class envelope mass
+// seg_mass[k] = wfirst[k] * len_k (one thread; K is small).  The hub plan
+// balances splits on envelope mass: the samplers' work is proportional to
+// proposals, i.e. to envelope mass, and no pass over w is needed.
+__global__ void segment_envelope_kernel(Segments seg, double* em, double* invwf, double* seg_mass) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double acc = 0.0;
   for (int k = 0; k < seg.K; ++k) {
     em[k] = acc;
     const double wf = seg.wfirst[k];
-    acc += wf * static_cast<double>(seg.start[k + 1] - seg.start[k]);
+    const double m = wf * static_cast<double>(seg.start[k + 1] - seg.start[k]);
+    seg_mass[k] = m;
+    acc += m;
     invwf[k] = wf > 0.0 ? 1.0 / wf : 0.0;
   }
   em[seg.K] = acc;
-}
-
-// seg_mass[k] = sum of w over segment k (any association; balance only).
-__global__ void segment_mass_kernel(const double* __restrict__ w, Segments seg, double* seg_mass) {
-  const int k = blockIdx.x;
-  if (k >= seg.K) return;
-  const int64_t a = seg.start[k], b = seg.start[k + 1];
-  double acc = 0.0;
-  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) acc += w[i];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CLG_FULL, acc, o);
-  __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
-    seg_mass[k] = t;
-  }
 }
 
 // bucket[b] = class holding envelope mass just below b * em[K] / kBuckets (a
