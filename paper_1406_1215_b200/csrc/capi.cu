@@ -160,7 +160,7 @@ struct clgen_dev_ctx {
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
-  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 8.0));
+  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 4.0));
   clg::LogTable* logtab = nullptr;  // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
@@ -625,13 +625,13 @@ int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in, int slot) {
 }
 
 // Heavy units (warp-cooperative kernel) then light units (lane-per-unit
-// kernel, occupancy variant CLGEN_CTR_MINB = 2|3|4, default 3).
+// kernel, occupancy variant CLGEN_CTR_MINB = 2|3|4, default 4: 64 registers).
 template <int MODE>
 int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
   static const int minb = [] {
     const char* e = std::getenv("CLGEN_CTR_MINB");
-    const int v = e ? std::atoi(e) : 3;
-    return v >= 2 && v <= 4 ? v : 3;
+    const int v = e ? std::atoi(e) : 4;
+    return v >= 2 && v <= 4 ? v : 4;
   }();
   clg::CtrWalkArgs a = a_in;
   const unsigned long long qstart[2] = {0ull, static_cast<unsigned long long>(c->ctr_heavy)};

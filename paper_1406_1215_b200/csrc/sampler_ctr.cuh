@@ -648,6 +648,15 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
 #endif
 constexpr int kLaneEvents = CLG_LANE_EVENTS;  // hazard events per lane iteration (light units)
 
+// lazy_accept with the unit stream key derived from (seed, u) only when the
+// 11 bits cannot decide (light units keep no key register)
+__device__ __forceinline__ bool lazy_accept_u(uint32_t h, double a, uint64_t seed_mix, uint32_t u, uint32_t id) {
+  const double s = a * 2048.0;
+  if (static_cast<double>(h + 1u) <= s) return true;
+  if (static_cast<double>(h) >= s) return false;
+  return lazy_accept(h, a, unit_key(seed_mix, u, 0), id);
+}
+
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                           const LogTable* __restrict__ logtab, uint64_t seed_mix) {
@@ -700,15 +709,16 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   // lane state (light units are plain sources whose hazard envelope starts
   // at u+1: the host routes hubs and sources with a pbar >= 1/16 band to the
   // warp kernel)
-  int64_t unit = -1, u = 0, out_pos = 0;
+  constexpr uint32_t kIdle = 0xffffffffu;
+  uint32_t u = kIdle;  // the lane's source (kIdle: none); its unit is u - lo - H + hub_units
+  int64_t out_pos = 0;
   int k = 0;
   int32_t cnt = 0;
-  uint64_t lkey = 0;
   uint32_t ev = 0;  // event serial of the unit's hazard process
   // proposals form a Poisson process of rate c_u * wfirst[k] per position,
   // i.e. unit rate in T = c_u * (envelope mass); T is tracked in
   // envelope-mass units (divided by c_u).
-  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0, hsc = 0.0, em_next = 0.0;
+  double T = 0.0, inv_c = 0.0, c_u = 0.0, inv_kappa = 0.0;
   // hs = floor(sure_k (2^11 / kappa) (1 - 2^-40)) <= floor(sure_k g_k 2^11)
   // (g_k >= 1/kappa): R < hs/2^11 accepts without w[v] and without g_k
   uint32_t hs = 0;
@@ -717,14 +727,14 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   // software-pipelined accept: an uncertain candidate's weight is loaded in
   // one iteration and compared in the next, so the warp never waits on it
   bool pend = false;
-  uint32_t pend_v = 0, pend_h = 0, pend_id = 0;
+  uint32_t pend_v = 0, pend_h = 0;  // pend_h: acceptance bits | event id << 11
   double pend_f = 0.0, pend_w = 0.0;
   Xoro128 rng;
 
   auto set_class = [&](int kn) {
     k = kn;
-    em_next = s_rec[kn + 1].em;
-    hs = kn < K ? static_cast<uint32_t>(static_cast<double>(s_suref[kn]) * hsc) : 0u;
+    hs = kn < K ? static_cast<uint32_t>(static_cast<double>(s_suref[kn]) * ((2048.0 * inv_kappa) * (1.0 - 0x1.0p-40)))
+                : 0u;
   };
   auto class_of = [&](double t) -> int {
     const double bt = t * a.seg.inv_bucket;
@@ -755,7 +765,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   const int64_t hub_units = a.H > 0 ? a.hub_units[a.H] : 0;
 
   for (;;) {
-    const unsigned need = __ballot_sync(CLG_FULL, unit < 0);
+    const unsigned need = __ballot_sync(CLG_FULL, u == kIdle);
     if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
       const int want = __popc(need);
       const int r = __popc(need & lt_mask);
@@ -780,16 +790,14 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         }
       }
       if (mine >= 0) {
-        unit = mine;
-        u = a.lo + a.H + (mine - hub_units);
+        u = static_cast<uint32_t>(a.lo + a.H + (mine - hub_units));
         cnt = 0;
         ev = 0;
         done = true;
         if (MODE == kWalkWrite) out_pos = a.offsets[mine];
         const double wu = w[u];
-        lkey = unit_key(seed_mix, u, 0);
-        rng.seed_key(lkey);
-        const int64_t j = u + 1;
+        rng.seed_key(unit_key(seed_mix, u, 0));
+        const int64_t j = static_cast<int64_t>(u) + 1;
         if (mine < hub_units || (j < a.n && !(wu * w[j] * a.invS < kBandTau * 0.999))) {
           atomicAdd(a.overflow, 1ull << 40);  // plan violation: not a light unit (reported as an error)
         } else if (j < a.n && S > 0.0 && wu > 0.0) {
@@ -803,7 +811,6 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
             c_u = kappa * (wu * a.invS);
             inv_c = __drcp_rn(c_u);
             inv_kappa = __drcp_rn(kappa);
-            hsc = (2048.0 * inv_kappa) * (1.0 - 0x1.0p-40);
             T = s_rec[kb].em + s_rec[kb].wf * static_cast<double>(j - static_cast<int64_t>(s_rec[kb].s0));
             prev_v = static_cast<uint32_t>(u);
             set_class(kb);
@@ -812,7 +819,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         }
       }
     }
-    const unsigned live = __ballot_sync(CLG_FULL, unit >= 0);
+    const unsigned live = __ballot_sync(CLG_FULL, u != kIdle);
     if (!live) {
       if (drained) break;
       continue;
@@ -827,14 +834,14 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     }
     bool finish = false;
     // resolve the candidate whose weight was requested last iteration
-    const bool acc_prev = pend && lazy_accept(pend_h, pend_w * pend_f, lkey, pend_id);
+    const bool acc_prev = pend && lazy_accept_u(pend_h & 2047u, pend_w * pend_f, seed_mix, u, pend_h >> 11);
     const uint32_t v_prev = pend_v;
     pend = false;
     bool pend_new = false;
     int pend_slot = -1;
     uint32_t pv_new = 0, ph_new = 0, pid_new = 0;
     double pf_new = 0.0;
-    if (unit >= 0) {
+    if (u != kIdle) {
       if (done) {
         finish = true;
       } else {
@@ -846,7 +853,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
           T += exp_bits(x, s_log) * inv_c;
           const uint32_t h = static_cast<uint32_t>(x) & 2047u;
           const uint32_t id = ev++;
-          if (!(T < em_next)) {
+          if (!(T < s_rec[k + 1].em)) {
             if (!(T < a.seg.em_end)) finish = true;
             else set_class(class_of(T));
           }
@@ -869,7 +876,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
                   pid_new = id;
                   pf_new = fk;
                 } else {  // second uncertain candidate of the iteration (rare): decide now
-                  acc[e] = lazy_accept(h, w[v_e] * fk, lkey, id);
+                  acc[e] = lazy_accept_u(h, w[v_e] * fk, seed_mix, u, id);
                 }
               }
             }
@@ -881,7 +888,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
         // the unit ends this iteration: an outstanding candidate must be
         // decided before the lane moves on to another unit
         if (finish && pend_new) {
-          const bool acc_p = lazy_accept(ph_new, w[pv_new] * pf_new, lkey, pid_new);
+          const bool acc_p = lazy_accept_u(ph_new, w[pv_new] * pf_new, seed_mix, u, pid_new);
 #pragma unroll
           for (int e = 0; e < kLaneEvents; ++e)
             if (e == pend_slot) acc[e] = acc_p;
@@ -895,8 +902,7 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
     if (pend_new) {
       pend = true;
       pend_v = pv_new;
-      pend_h = ph_new;
-      pend_id = pid_new;
+      pend_h = ph_new | (pid_new << 11);
       pend_f = pf_new;
       pend_w = w[pv_new];
     }
@@ -925,11 +931,11 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
       if (kLaneEvents & 1)
         fs.emit2(a, u32, tmask, lt_mask, lane, acc[kLaneEvents - 1], vv[kLaneEvents - 1], false, 0u);
     }
-    if (unit >= 0 && finish) {
-      if (MODE == kWalkCount) a.counts[unit] = cnt;
-      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
-        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
-      unit = -1;
+    if (u != kIdle && finish) {
+      if (MODE == kWalkCount) a.counts[static_cast<int64_t>(u) - a.lo - a.H + hub_units] = cnt;
+      if (MODE == kWalkFold && a.degree && (static_cast<int64_t>(u) & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+        atomicAdd(&a.degree[static_cast<int64_t>(u) >> a.track_shift], static_cast<uint32_t>(cnt));
+      u = kIdle;
     }
   }
 
