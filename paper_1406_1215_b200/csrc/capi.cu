@@ -604,7 +604,6 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
   a.queue = &c->sc->queue;
   a.overflow = &c->sc->overflow;
   a.fold_out = c->sc->fold;
-  a.ring_head = &c->sc->ring_head;
   return a;
 }
 

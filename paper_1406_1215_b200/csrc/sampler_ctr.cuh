@@ -76,7 +76,6 @@ struct CtrWalkArgs {
   int track_shift;
   uint2* ring;
   unsigned long long ring_mask;
-  unsigned long long* ring_head;
   unsigned long long* fold_out;
   unsigned long long* overflow;
   WarpProf prof;
@@ -117,7 +116,6 @@ __device__ __forceinline__ uint64_t unit_key(uint64_t seed_mix, int64_t u, uint3
   return mix64(seed_mix ^ (static_cast<uint64_t>(u) | (static_cast<uint64_t>(split) << 36)));
 }
 
-enum CtrPhase : int { kPhSat = 0, kPhBand = 1, kPhHaz = 2 };
 
 
 // ---- warp-cooperative processing of heavy units --------------------------
