@@ -260,6 +260,26 @@ __host__ __device__ inline size_t ctr_warp_smem_bytes(int K, int nb, int threads
          static_cast<size_t>(threads / 32) * kSideCap * sizeof(uint32_t);
 }
 
+// Per-warp unit constants of the warp kernel, kept in shared memory instead
+// of registers (read at class-window refreshes and rare slow paths only).
+struct WarpUnitConst {
+  double c_u, inv_kappa;
+  uint64_t ukey;  // unit stream key; lane l's key is ukey + C (l + 1)
+};
+
+__device__ __forceinline__ uint64_t lane_key(uint64_t ukey, int lane) {
+  return ukey + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1);
+}
+
+// lazy_accept with the lane's key read from shared memory only when the 11
+// bits cannot decide
+__device__ __forceinline__ bool lazy_accept_w(uint32_t h, double a, const WarpUnitConst& wc, int lane, uint32_t id) {
+  const double s = a * 2048.0;
+  if (static_cast<double>(h + 1u) <= s) return true;
+  if (static_cast<double>(h) >= s) return false;
+  return lazy_accept(h, a, lane_key(wc.ukey, lane), id);
+}
+
 template <int MODE, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                               const LogTable* __restrict__ logtab, uint64_t seed_mix,
@@ -297,6 +317,8 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
 
   const int lane = lane_id();
   uint32_t* side = s_side + (threadIdx.x >> 5) * kSideCap;
+  __shared__ WarpUnitConst s_wc[THREADS / 32];
+  WarpUnitConst& wc = s_wc[threadIdx.x >> 5];
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const unsigned lt_mask = lanemask_lt();
   const double* __restrict__ w = a.w;
@@ -335,8 +357,10 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
     int64_t out_pos = MODE == kWalkWrite ? a.offsets[unit] : 0;
     int32_t cnt = 0;
     // lane streams: key(u, split) mixed with the lane
-    const uint64_t lkey = unit_key(seed_mix, u, split) + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1);
-    rng.seed_key(lkey);
+    const uint64_t ukey = unit_key(seed_mix, u, split);
+    rng.seed_key(lane_key(ukey, lane));
+    __syncwarp();
+    if (lane == 0) wc.ukey = ukey;
 
     // emission of up to two edges per lane, lane-major (c0 before c1)
     auto emit2 = [&](bool c0, uint32_t v0, bool c1, uint32_t v1) {
@@ -467,9 +491,12 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
           double kappa = 1.0 / 17.0;
 #pragma unroll
           for (int t = 16; t >= 1; --t) kappa = __fma_rn(kappa, ymax, 1.0 / static_cast<double>(t));
-          const double c_u = kappa * (wu * a.invS);
-          const double inv_c = __drcp_rn(c_u);
-          const double inv_kappa = __drcp_rn(kappa);
+          const double inv_c = __drcp_rn(kappa * (wu * a.invS));
+          if (lane == 0) {
+            wc.c_u = kappa * (wu * a.invS);
+            wc.inv_kappa = __drcp_rn(kappa);
+          }
+          __syncwarp();
           double T0 = s_rec[k].em + s_rec[k].wf * static_cast<double>(vB - static_cast<int64_t>(s_rec[k].s0));
           uint32_t prev_v = static_cast<uint32_t>(vB - 1);
           const uint32_t vend32 = static_cast<uint32_t>(vend);
@@ -484,7 +511,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
           auto refresh = [&]() {
             const int kc = kw + lane;
             if (kc < K) {
-              g_lane = bern_gk(inv_kappa, c_u * s_rec[kc].wf);
+              g_lane = bern_gk(wc.inv_kappa, wc.c_u * s_rec[kc].wf);
               hs_lane = static_cast<uint32_t>((__ldg(g_sure + kc) * g_lane) * 2048.0);
             } else {
               g_lane = 0.0;
@@ -515,7 +542,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
             return kl;
           };
           for (;;) {
-            const bool accp = kDefer && pend && lazy_accept(ph & 0xffffu, pw * pf, lkey, ev - 2 + (ph >> 16));
+            const bool accp = kDefer && pend && lazy_accept_w(ph & 0xffffu, pw * pf, wc, lane, ev - 2 + (ph >> 16));
             const uint32_t pvv = pv;
             pend = false;
             const uint64_t xa = rng.next(), xb = rng.next();
@@ -554,7 +581,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
               double gb = __shfl_sync(CLG_FULL, g_lane, dib & 31);
               if (unca) {
                 if (dia >= 32) {
-                  ga = bern_gk(inv_kappa, c_u * s_rec[kla].wf);
+                  ga = bern_gk(wc.inv_kappa, wc.c_u * s_rec[kla].wf);
                   hsa = static_cast<uint32_t>((__ldg(g_sure + kla) * ga) * 2048.0);
                 }
                 if (ha < hsa) {
@@ -568,13 +595,13 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
                     pf = f;
                     pw = w[va];  // consumed next round
                   } else {
-                    acca2 = lazy_accept(ha, w[va] * f, lkey, ev);
+                    acca2 = lazy_accept_w(ha, w[va] * f, wc, lane, ev);
                   }
                 }
               }
               if (uncb) {
                 if (dib >= 32) {
-                  gb = bern_gk(inv_kappa, c_u * s_rec[klb].wf);
+                  gb = bern_gk(wc.inv_kappa, wc.c_u * s_rec[klb].wf);
                   hsb = static_cast<uint32_t>((__ldg(g_sure + klb) * gb) * 2048.0);
                 }
                 if (hb < hsb) {
@@ -588,7 +615,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
                     pf = f;
                     pw = w[vb];
                   } else {  // write mode, or a second uncertain event this round (rare): decide now
-                    accb2 = lazy_accept(hb, w[vb] * f, lkey, ev + 1);
+                    accb2 = lazy_accept_w(hb, w[vb] * f, wc, lane, ev + 1);
                   }
                 }
               }
@@ -600,7 +627,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
             // carry the last lane's second event into the next round
             if (!__all_sync(CLG_FULL, validb)) {
               if (kDefer) {
-                const bool lp = pend && lazy_accept(ph & 0xffffu, pw * pf, lkey, ev - 2 + (ph >> 16));
+                const bool lp = pend && lazy_accept_w(ph & 0xffffu, pw * pf, wc, lane, ev - 2 + (ph >> 16));
                 if (MODE == kWalkFold) side_push(lp, pv, false, 0u);
                 else emit2(lp, pv, false, 0u);
               }
