@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
 // the warp kernel; every draw comes from the unit's own stream, in event
 // order, so the count, write and fold modes make identical decisions.
 #ifndef CLG_LANE_EVENTS
-#define CLG_LANE_EVENTS 3
+#define CLG_LANE_EVENTS 4
 #endif
 constexpr int kLaneEvents = CLG_LANE_EVENTS;  // hazard events per lane iteration (light units)
 
