@@ -108,7 +108,8 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
  * w_last inside a class; default 1/64) and the hub split size in expected
- * candidates (default 8192).  Changing them changes the generated graph. */
+ * candidates (0 = automatic, the default: S / 2^17 clamped to [1024, 8192],
+ * a function of the weights only).  Changing them changes the generated graph. */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);
 /* Reference stream arithmetic: 1 (default) = fast guarded FP64 (table log,
  * series log1p, FMA-certified divisions; falls back to the reference

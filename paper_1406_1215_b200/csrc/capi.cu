@@ -139,8 +139,9 @@ struct clgen_dev_ctx {
   double seg_em_end = 0.0;     // envelope mass em[K]
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
-  double split_cap = env_double("CLGEN_CTR_SPLIT", 8192.0);
+  double split_cap = env_double("CLGEN_CTR_SPLIT", 0.0);  // 0: auto (effective_split_cap)
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
+  double ctr_S = 0.0;  // S the cached hub plan was built for
   double heavy_cand = env_double("CLGEN_CTR_HEAVY", 384.0);  // units with >= this many expected candidates run warp-cooperatively
   DevBuf probe;
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -492,12 +493,23 @@ clg::Segments segments(clgen_dev_ctx* c) {
 
 // Hub split plan for sources [lo,hi): sources whose envelope-expected
 // candidate count exceeds split_cap are split into v-ranges of ~split_cap.
+// The automatic cap is a function of the weights only (S, so every rank and
+// every partition of the sources uses the same plan): S/2 bounds the expected
+// edge count, and splits of 1/2^16 of it, clamped to [1024, 8192] expected
+// candidates, keep small graphs balanced and large ones cheap per unit.
+double effective_split_cap(const clgen_dev_ctx* c, double S) {
+  if (c->split_cap > 0.0) return c->split_cap;
+  const double cap = S / 131072.0;
+  return cap < 1024.0 ? 1024.0 : (cap > 8192.0 ? 8192.0 : cap);
+}
+
 int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
   int rc = ensure_segments(c);
   if (rc) return rc;
-  if (c->ctr_lo == lo && c->ctr_hi == hi) return CLGEN_OK;
+  if (c->ctr_lo == lo && c->ctr_hi == hi && c->ctr_S == S) return CLGEN_OK;
   // E_u <= w_u (1+eps): only sources with w_u >= cap/(1+eps) can be hubs
-  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, lo, hi, c->split_cap / (1.0 + 2.0 * c->seg_eps),
+  const double split_cap = effective_split_cap(c, S);
+  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, lo, hi, split_cap / (1.0 + 2.0 * c->seg_eps),
                                                    reinterpret_cast<long long*>(&c->sc->total));
   ++c->launches;
   CUDA_TRY(cudaGetLastError());
@@ -513,7 +525,7 @@ int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
     int64_t* splits = reinterpret_cast<int64_t*>(c->counts.p);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((H + 255) / 256, c->num_sms * 8));
     clg::hub_splits_kernel<<<grid, 256, 0, c->stream>>>(c->w, c->n, S, lo, H, segments(c), c->seg_mass.as<double>(),
-                                                      c->split_cap, splits);
+                                                      split_cap, splits);
     ++c->launches;
     CUDA_TRY(cudaGetLastError());
     // exclusive scan of split counts -> hub_units[0..H), total -> hub_units[H]
@@ -582,6 +594,7 @@ int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
     c->ctr_heavy = hub_total + (std::max<int64_t>(lo_b, pure0) - a0);
   }
   c->ctr_lo = lo;
+  c->ctr_S = S;
   c->ctr_hi = hi;
   return CLGEN_OK;
 }
@@ -1310,7 +1323,7 @@ int clgen_dev_generate_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi,
 int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double split_cap) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (!(class_eps > 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be in (0,1]");
-  if (!(split_cap >= 32.0)) return fail(CLGEN_EINVAL, "split_cap must be >= 32");
+  if (!(split_cap == 0.0 || split_cap >= 32.0)) return fail(CLGEN_EINVAL, "split_cap must be 0 (auto) or >= 32");
   c->seg_eps = class_eps;
   c->split_cap = split_cap;
   c->seg_valid = false;
