@@ -107,7 +107,7 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
                              int64_t* n_flagged);
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
- * w_last inside a class; default 1/64) and the hub split size in expected
+ * w_last inside a class; default 1/128, doubled until at most 1024 classes) and the hub split size in expected
  * candidates (0 = automatic, the default: S / 2^17 clamped to [1024, 8192],
  * a function of the weights only).  Changing them changes the generated graph. */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);

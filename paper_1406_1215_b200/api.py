@@ -136,7 +136,7 @@ class Device:
         check(_lib.lib().clgen_dev_blocked_sum(self._h, C.byref(out)))
         return out.value
 
-    def set_counter_params(self, class_eps: float = 1.0 / 64, split_cap: float = 0.0) -> None:
+    def set_counter_params(self, class_eps: float = 1.0 / 128, split_cap: float = 0.0) -> None:
         """Counter-stream weight-class width and hub split size (changes the graph)."""
         check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, split_cap))
 

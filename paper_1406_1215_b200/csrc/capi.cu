@@ -138,7 +138,7 @@ struct clgen_dev_ctx {
   int seg_nb = clg::kBuckets;  // buckets in the class index
   double seg_em_end = 0.0;     // envelope mass em[K]
   bool seg_valid = false;
-  double seg_eps = env_double("CLGEN_CTR_EPS", 0.015625);
+  double seg_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 0.0);  // 0: auto (effective_split_cap)
   int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
   double ctr_S = 0.0;  // S the cached hub plan was built for
@@ -147,6 +147,7 @@ struct clgen_dev_ctx {
   int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   int ctr_warp_blocks[3] = {0, 0, 0};
   size_t ctr_warp_smem[3] = {0, 0, 0};
+  size_t ctr_walk_smem[3][3] = {};
   int ctr_warp_cfg[3] = {-1, -1, -1};
   int warp_cfg = -1;       // clgen_dev_set_kernel_shape (-1: CLGEN_WARP_CFG / default)
   bool force_deep = false;  // class lookup by forward walk (test hook)
@@ -623,13 +624,18 @@ clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, ui
 template <int MODE, int MINB>
 int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in, int slot) {
   clg::CtrWalkArgs a = a_in;
-  if (!c->ctr_blocks[slot][MODE]) {
+  const size_t smem = clg::ctr_walk_smem_bytes(c->seg_K, c->seg_nb);
+  if (!c->ctr_blocks[slot][MODE] || c->ctr_walk_smem[slot][MODE] != smem) {
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(clg::ctr_walk_kernel<MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, 0));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, smem));
     c->ctr_blocks[slot][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    c->ctr_walk_smem[slot][MODE] = smem;
   }
   a.prof = prof_slots(c, c->ctr_blocks[slot][MODE], c->ctr_heavy == 0);
-  clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, 0, c->stream>>>(
+  clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, smem, c->stream>>>(
       a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix);
   CUDA_TRY(cudaGetLastError());
   ++c->launches;
@@ -669,6 +675,8 @@ int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
     const size_t smem = clg::ctr_warp_smem_bytes(c->seg_K, c->seg_nb, threads);
     auto launch = [&](auto kern) -> int {
       if (!c->ctr_warp_blocks[MODE] || c->ctr_warp_smem[MODE] != smem || c->ctr_warp_cfg[MODE] != wcfg) {
+        if (smem > 48 * 1024)
+          CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;

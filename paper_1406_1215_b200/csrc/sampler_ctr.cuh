@@ -52,7 +52,7 @@ struct Segments {
 
 constexpr int kBuckets = 8192;  // bucket table capacity
 
-constexpr int kSegSmemMax = 640;  // classes staged in shared memory per CTA (static smem < 48 KB)
+constexpr int kSegSmemMax = 1024;  // classes staged in (dynamic) shared memory per CTA
 constexpr double kBandTau = 0.0625;  // hazard envelope below pbar = 1/16
 
 struct CtrWalkArgs {
@@ -682,16 +682,28 @@ __device__ __forceinline__ bool lazy_accept_u(uint32_t h, double a, uint64_t see
   return lazy_accept(h, a, unit_key(seed_mix, u, 0), id);
 }
 
+// Dynamic shared memory of the light-unit kernel: K+2 class records, the log
+// table, the bucket index, the float sure bounds and the per-warp staging of
+// deferred accepts (u, v).
+__host__ __device__ inline size_t ctr_walk_smem_bytes(int K, int nb) {
+  return static_cast<size_t>(K + 2) * sizeof(ClassRec) + sizeof(LogTable) +
+         ((static_cast<size_t>(nb) * sizeof(unsigned short) + 15) & ~size_t(15)) +
+         ((static_cast<size_t>(K) * sizeof(float) + 15) & ~size_t(15)) + (256 / 32) * 64 * sizeof(uint2);
+}
+
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, const int64_t* __restrict__ split_pos,
                                                           const LogTable* __restrict__ logtab, uint64_t seed_mix) {
   constexpr int64_t kBatch = 32;
-  __shared__ ClassRec s_rec[kSegSmemMax + 2];
-  __shared__ LogTable s_log;
-  __shared__ unsigned short s_bucket[kBuckets];
-  __shared__ uint2 s_side[256 / 32][64];  // fold mode: deferred accepts (u, v), folded 32 at a time
-  __shared__ float s_suref[kSegSmemMax];   // sure_k rounded down to float
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.seg.K;
+  ClassRec* s_rec = reinterpret_cast<ClassRec*>(smem_raw);
+  LogTable& s_log = *reinterpret_cast<LogTable*>(smem_raw + static_cast<size_t>(K + 2) * sizeof(ClassRec));
+  unsigned short* s_bucket = reinterpret_cast<unsigned short*>(reinterpret_cast<unsigned char*>(&s_log) + sizeof(LogTable));
+  float* s_suref = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(s_bucket) +
+                                            ((static_cast<size_t>(a.seg.nb) * sizeof(unsigned short) + 15) & ~size_t(15)));
+  uint2 (*s_side)[64] = reinterpret_cast<uint2 (*)[64]>(reinterpret_cast<unsigned char*>(s_suref) +
+                                                        ((static_cast<size_t>(K) * sizeof(float) + 15) & ~size_t(15)));
   for (int i = threadIdx.x; i < K; i += blockDim.x) s_suref[i] = __double2float_rd(a.seg.sure[i]);
   for (int i = threadIdx.x; i <= K; i += blockDim.x) {
     ClassRec r;
