@@ -230,7 +230,11 @@ struct FoldSink {
   }
 };
 
-constexpr int kSideCap = 128;  // per-warp staging of deferred accepts (fold mode)
+constexpr int kSideCap = 128;
+#ifndef CLG_WIN_REFRESH
+#define CLG_WIN_REFRESH 16
+#endif
+constexpr int kWinRefresh = CLG_WIN_REFRESH;  // slide the 32-class acceptance window when the round reached class kw + this  // per-warp staging of deferred accepts (fold mode)
 
 // Class record staged in shared memory: everything an event needs to map its
 // envelope mass T to a position in class k (two 16-byte loads).
@@ -636,7 +640,7 @@ __global__ void __launch_bounds__(THREADS, MINB) ctr_warp_kernel(CtrWalkArgs a, 
             T0 = __shfl_sync(CLG_FULL, Tb, 31);
             k = __shfl_sync(CLG_FULL, klb, 31);
             prev_v = __shfl_sync(CLG_FULL, vb, 31);
-            if (k - kw >= 16) {
+            if (k - kw >= kWinRefresh) {
               kw = k;
               refresh();
             }
