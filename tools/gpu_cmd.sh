@@ -1,4 +1,7 @@
-rm -f gpurun_out/sweep.txt
-bash tools/sweep.sh "--config c4 --steps 2 --warmup 3" "CLGEN_CTR_HEAVY=256" "CLGEN_CTR_HEAVY=384" "CLGEN_CTR_HEAVY=512" "CLGEN_CTR_HEAVY=256 CLGEN_CTR_SPLIT=8192" "CLGEN_CTR_HEAVY=384 CLGEN_CTR_SPLIT=8192"
-bash tools/sweep.sh "--config c3 --steps 5 --warmup 3" "X=1" "CLGEN_CTR_HEAVY=256" "CLGEN_CTR_HEAVY=384"
-bash tools/sweep.sh "--config c5 --steps 5 --warmup 3" "X=1" "CLGEN_CTR_HEAVY=256" "CLGEN_CTR_HEAVY=384"
+bash tools/round_measure.sh
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv \
+    --log-file gpurun_out/c4_bench_launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/c4_ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:ctr_warp_kernel -c 1 \
+    -o gpurun_out/c4_ctr_warp_full python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/c4_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:ctr_walk_kernel -c 1 \
+    -o gpurun_out/c4_ctr_walk_full python bench.py --num-vertices 200000000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/c4_ncu_walk.log 2>&1
