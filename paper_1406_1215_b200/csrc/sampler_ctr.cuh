@@ -994,24 +994,71 @@ __global__ void __launch_bounds__(256, MINB) ctr_walk_kernel(CtrWalkArgs a, cons
   if (MODE == kWalkFold) fs.finish(a, lane);
 }
 
-// Envelope-expected candidate count of source u over [u+1, n) (the same
-// estimate that sizes hub splits); non-increasing in u.
+// Envelope-expected candidate count of source u over [u+1, n), in closed
+// form from the envelope-mass prefix (O(log K) per source): positions in
+// classes with w_u wfirst_k / S >= 1 (a prefix of the classes) count 1 each,
+// the rest (w_u / S) x envelope mass.  The hub split plan and the heavy/light
+// choice use it; both are functions of the weights only.
+struct HubExpect {
+  double sat;    // saturated positions in [u+1, n)
+  double scale;  // w_u / S
+  double Ta;     // envelope coordinate where the unsaturated part starts
+  int64_t a;     // first unsaturated position (>= u+1)
+  double E;      // total expected candidates
+};
+
+// envelope coordinate of node p in [0, n]: em[k] + wfirst_k (p - start_k)
+__device__ __forceinline__ double env_coord(const Segments& seg, int64_t p) {
+  if (p >= seg.start[seg.K]) return seg.em[seg.K];
+  const int k = seg_of(seg, p);
+  return seg.em[k] + seg.wfirst[k] * static_cast<double>(p - seg.start[k]);
+}
+
+__device__ __forceinline__ HubExpect hub_expect(const Segments& seg, double wu, int64_t u, double S) {
+  HubExpect h{0.0, 0.0, 0.0, u + 1, 0.0};
+  const int64_t n = seg.start[seg.K];
+  if (u + 1 >= n || !(wu > 0.0) || !(S > 0.0)) return h;
+  int lo = -1, hi = seg.K;  // first class with pbar < 1 in (lo, hi]
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (pbar_of(wu, seg.wfirst[m], S) < 1.0) hi = m; else lo = m;
+  }
+  const int64_t sks = seg.start[hi];
+  h.a = sks > u + 1 ? sks : u + 1;
+  h.sat = static_cast<double>(h.a - (u + 1));
+  h.scale = wu / S;
+  h.Ta = env_coord(seg, h.a);
+  h.E = h.sat + h.scale * (seg.em[seg.K] - h.Ta);
+  return h;
+}
+
+// first position p >= u+1 where the expected count over [u+1, p) reaches t
+__device__ __forceinline__ int64_t hub_position(const Segments& seg, const HubExpect& h, int64_t u, double t) {
+  const int64_t n = seg.start[seg.K];
+  if (t <= h.sat) {
+    const int64_t p = u + 1 + static_cast<int64_t>(t);
+    return p < h.a ? p : h.a;
+  }
+  const double T = h.Ta + (t - h.sat) / h.scale;
+  if (!(T < seg.em[seg.K])) return n;
+  int lo = 0, hi = seg.K;  // em[lo] <= T < em[hi]
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (seg.em[m] <= T) lo = m; else hi = m;
+  }
+  const double wf = seg.wfirst[lo];
+  int64_t p = seg.start[lo] + (wf > 0.0 ? static_cast<int64_t>((T - seg.em[lo]) / wf) : 0);
+  if (p > seg.start[lo + 1]) p = seg.start[lo + 1];
+  if (p < h.a) p = h.a;
+  return p;
+}
+
 __device__ __forceinline__ double expected_candidates(const double* __restrict__ w, int64_t n, double S,
                                                       const Segments& seg, const double* __restrict__ seg_mass,
                                                       int64_t u) {
-  const double wu = w[u];
-  double E = 0.0;
-  if (u + 1 < n && wu > 0.0) {
-    for (int k = seg_of(seg, u + 1); k < seg.K; ++k) {
-      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
-      const int64_t b = seg.start[k + 1];
-      if (b <= a) continue;
-      const double pb = wu * seg.wfirst[k] / S;
-      E += pb >= 1.0 ? static_cast<double>(b - a)
-                     : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
-    }
-  }
-  return E;
+  (void)n;
+  (void)seg_mass;
+  return hub_expect(seg, w[u], u, S).E;
 }
 
 // out[i] = expected_candidates(us[i])
@@ -1070,26 +1117,13 @@ __global__ void build_segments_kernel(const double* __restrict__ w, int64_t n, d
 }
 
 // Hub split plan: for source u in [lo, lo+Hmax) the expected candidate count
-// over [u+1, n) under the segment envelope; split count = ceil(E / cap).
+// over [u+1, n) under the class envelope; split count = ceil(E / cap).
 __global__ void hub_splits_kernel(const double* __restrict__ w, int64_t n, double S, int64_t lo, int64_t Hmax,
                                   Segments seg, const double* __restrict__ seg_mass, double cap,
                                   int64_t* splits) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < Hmax; i += stride) {
-    const int64_t u = lo + i;
-    const double wu = w[u];
-    double E = 0.0;
-    if (u + 1 < n && wu > 0.0) {
-      int k = seg_of(seg, u + 1);
-      for (; k < seg.K; ++k) {
-        const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
-        const int64_t b = seg.start[k + 1];
-        if (b <= a) continue;
-        const double pb = wu * seg.wfirst[k] / S;
-        if (pb >= 1.0) E += static_cast<double>(b - a);
-        else E += wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
-      }
-    }
+    const double E = expected_candidates(w, n, S, seg, seg_mass, lo + i);
     const double s = ceil(E / cap);
     splits[i] = s < 1.0 ? 1 : static_cast<int64_t>(s);
   }
@@ -1097,48 +1131,25 @@ __global__ void hub_splits_kernel(const double* __restrict__ w, int64_t n, doubl
 
 // Split positions of every hub unit: split s of hub u covers
 // [pos(s), pos(s+1)) with pos chosen so each share carries E/splits expected
-// candidates (segment-level mass, positions interpolated inside a segment).
+// candidates (closed form, positions interpolated inside a class).
 __global__ void hub_positions_kernel(const double* __restrict__ w, int64_t n, double S, int64_t lo, int64_t H,
                                      Segments seg, const double* __restrict__ seg_mass,
                                      const int64_t* __restrict__ hub_units, int64_t* pos) {
+  (void)seg_mass;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < H; i += stride) {
     const int64_t u = lo + i;
-    const double wu = w[u];
     const int64_t u0 = hub_units[i], ns = hub_units[i + 1] - u0;
-    // total expected candidates
-    const int k0 = seg_of(seg, u + 1);
-    double E = 0.0;
-    for (int k = k0; k < seg.K; ++k) {
-      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
-      const int64_t b = seg.start[k + 1];
-      if (b <= a) continue;
-      const double pb = wu * seg.wfirst[k] / S;
-      E += pb >= 1.0 ? static_cast<double>(b - a)
-                     : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
+    const HubExpect h = hub_expect(seg, w[u], u, S);
+    int64_t prev = u + 1;
+    pos[u0] = prev;
+    for (int64_t s = 1; s < ns; ++s) {
+      int64_t p = hub_position(seg, h, u, h.E * static_cast<double>(s) / static_cast<double>(ns));
+      if (p < prev) p = prev;
+      if (p > n) p = n;
+      pos[u0 + s] = p;
+      prev = p;
     }
-    pos[u0] = u + 1;
-    int64_t s = 1;
-    double acc = 0.0;
-    for (int k = k0; k < seg.K && s < ns; ++k) {
-      const int64_t a = seg.start[k] < u + 1 ? u + 1 : seg.start[k];
-      const int64_t b = seg.start[k + 1];
-      if (b <= a) continue;
-      const double pb = wu * seg.wfirst[k] / S;
-      const double e = pb >= 1.0 ? static_cast<double>(b - a)
-                                 : wu * (a == seg.start[k] ? seg_mass[k] : seg.wfirst[k] * static_cast<double>(b - a)) / S;
-      while (s < ns && acc + e >= E * static_cast<double>(s) / static_cast<double>(ns)) {
-        const double frac = e > 0.0 ? (E * static_cast<double>(s) / static_cast<double>(ns) - acc) / e : 0.0;
-        int64_t p = a + static_cast<int64_t>(frac * static_cast<double>(b - a));
-        if (p < a) p = a;
-        if (p > b) p = b;
-        if (p <= pos[u0 + s - 1]) p = pos[u0 + s - 1];
-        pos[u0 + s] = p;
-        ++s;
-      }
-      acc += e;
-    }
-    for (; s < ns; ++s) pos[u0 + s] = n;
   }
 }
 
