@@ -132,11 +132,13 @@ struct clgen_dev_ctx {
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
   // counter stream: weight-class segment table (per weights) and the hub
   // split plan of the last source range
+  DevBuf grid_thr, grid_bounds;  // class grid thresholds / boundaries (ensure_segments)
   DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
   int seg_K = 0;
   int seg_depth = 64;  // bucket lookup depth (segment_buckets_kernel)
   int seg_nb = clg::kBuckets;  // buckets in the class index
   double seg_em_end = 0.0;     // envelope mass em[K]
+  double seg_eps_used = 0.0;   // class width after doubling to fit the cap
   bool seg_valid = false;
   double seg_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
   double split_cap = env_double("CLGEN_CTR_SPLIT", 0.0);  // 0: auto (effective_split_cap)
@@ -445,16 +447,57 @@ int ensure_segments(clgen_dev_ctx* c) {
   CUDA_TRY(c->seg_em.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_invwf.ensure((kmax + 1) * sizeof(double)));
   CUDA_TRY(c->seg_bucket.ensure(clg::kBuckets * sizeof(unsigned short)));
+  // zero weights start at z; the positive range is [w[z-1], w[0]]
+  double tiny;  // smallest positive double: w < tiny <=> w == 0 for non-negative weights
+  {
+    const long long one = 1;
+    std::memcpy(&tiny, &one, sizeof tiny);
+  }
+  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, 0, c->n, tiny,
+                                                   reinterpret_cast<long long*>(&c->sc->total));
+  ++c->launches;
+  CUDA_TRY(cudaGetLastError());
+  long long z = 0;
+  CUDA_TRY(cudaMemcpyAsync(&z, &c->sc->total, sizeof z, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  double wmax = 0.0, wmin = 0.0;
+  if (z > 0) {
+    CUDA_TRY(cudaMemcpy(&wmax, c->w, sizeof(double), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&wmin, c->w + (z - 1), sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  // grid width: the requested eps, doubled until the grid fits the class cap
   double eps = c->seg_eps;
-  for (int attempt = 0; attempt < 12; ++attempt, eps *= 2.0) {
-    clg::build_segments_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, eps, kmax, c->seg_start.as<int64_t>(),
-                                                        c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
-                                                        reinterpret_cast<int*>(&c->sc->total));
-    ++c->launches;
+  const int zero_class = z < c->n ? 1 : 0;
+  int kg = 0;
+  for (int attempt = 0; attempt < 40; ++attempt, eps *= 2.0) {
+    const double cells = z > 0 ? std::ceil(std::log(wmax / wmin) / std::log1p(eps)) + 1.0 : 0.0;
+    if (cells + zero_class <= kmax) {
+      kg = static_cast<int>(cells);
+      break;
+    }
+  }
+  if (z > 0 && kg == 0) return fail(CLGEN_EINVAL, "counter stream: weight range too wide for the class table");
+  {
+    std::vector<double> thr(kg + 1, 0.0);
+    double t = wmax;
+    for (int k = 1; k < kg; ++k) thr[k] = (t = t / (1.0 + eps));
+    CUDA_TRY(c->grid_thr.ensure((kg + 2) * sizeof(double)));
+    CUDA_TRY(c->grid_bounds.ensure((kg + 2) * sizeof(int64_t)));
+    CUDA_TRY(cudaMemcpyAsync(c->grid_thr.p, thr.data(), (kg + 1) * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    clg::grid_bounds_kernel<<<(kg + 1 + 255) / 256, 256, 0, c->stream>>>(c->w, z, c->grid_thr.as<double>(), kg,
+                                                                        c->grid_bounds.as<int64_t>());
+    clg::grid_compact_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, z, c->grid_bounds.as<int64_t>(), kg, kmax,
+                                                     c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(),
+                                                     c->seg_sure.as<double>(), reinterpret_cast<int*>(&c->sc->total));
+    c->launches += 2;
     CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // thr is a host vector
+  }
+  {
     int K = 0;
     CUDA_TRY(cudaMemcpyAsync(&K, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->seg_eps_used = eps;
     if (K > 0) {
       c->seg_K = K;
       clg::Segments sg = segments(c);
@@ -989,6 +1032,8 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->seg_em.release();
   c->seg_invwf.release();
   c->seg_bucket.release();
+  c->grid_thr.release();
+  c->grid_bounds.release();
   c->hub_units.release();
   c->split_pos.release();
   c->unit_counts.release();

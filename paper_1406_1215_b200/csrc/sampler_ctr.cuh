@@ -1072,48 +1072,52 @@ __global__ void expected_candidates_kernel(const double* __restrict__ w, int64_t
 }
 
 // ---- segment table -------------------------------------------------------
-// Segment boundaries: c_0 = 0; c_{k+1} = first j > c_k with
-// w[j] * (1+eps) < w[c_k]  (or with w[j] == 0 when w[c_k] > 0).  One warp:
-// lanes probe 32 candidate positions per bisection round.
-__global__ void build_segments_kernel(const double* __restrict__ w, int64_t n, double eps, int kmax,
-                                      int64_t* start, double* wfirst, double* sure, int* K_out) {
-  const int lane = threadIdx.x;
-  int64_t c = 0;
+// Classes on a geometric grid anchored at w[0]: thresholds t_k = w[0] /
+// (1+eps)^k (t_0 = +inf); class k holds the positive weights in
+// [t_{k+1}, t_k), so w[c_k] < (1+eps) w[c_{k+1}-1] holds by construction;
+// empty grid cells are dropped and zero weights form one last class.  Every
+// boundary is an independent binary search (one thread per grid cell), so
+// the table costs ~log2(n) dependent loads instead of a sequential walk.
+__global__ void grid_bounds_kernel(const double* __restrict__ w, int64_t z, const double* __restrict__ thr, int kg,
+                                   int64_t* bounds) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > kg) return;
+  if (k == 0) { bounds[0] = 0; return; }
+  if (k == kg) { bounds[kg] = z; return; }
+  const double t = thr[k];
+  int64_t lo = -1, hi = z;  // first j in [0, z) with w[j] < t, in (lo, hi]
+  while (hi - lo > 1) {
+    const int64_t m = lo + ((hi - lo) >> 1);
+    if (w[m] < t) hi = m; else lo = m;
+  }
+  bounds[k] = hi;
+}
+
+// Compact the non-empty grid cells into classes (one thread; kg <= a few
+// thousand) and append the zero class [z, n); K_out = number of classes.
+__global__ void grid_compact_kernel(const double* __restrict__ w, int64_t n, int64_t z,
+                                    const int64_t* __restrict__ bounds, int kg, int kmax, int64_t* start,
+                                    double* wfirst, double* sure, int* K_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int K = 0;
-  while (c < n && K < kmax) {
-    const double wc = w[c];
-    const double lim = wc > 0.0 ? wc / (1.0 + eps) : -1.0;  // next class: w < lim (zero class: never)
-    // first j in (c, n) with w[j] < lim, n if none; invariant: answer in (lo, hi]
-    int64_t lo = c, hi = n;
-    while (hi - lo > 1) {
-      const int64_t span = hi - lo - 1;
-      const int64_t step = (span + 31) / 32;
-      const int64_t p = lo + 1 + static_cast<int64_t>(lane) * step;
-      const bool below = p >= hi || w[p] < lim;
-      const unsigned m = __ballot_sync(CLG_FULL, below);
-      if (m == 0) {
-        lo = lo + 1 + 31 * step;
-        continue;
-      }
-      const int f = __ffs(m) - 1;
-      const int64_t pf = lo + 1 + static_cast<int64_t>(f) * step;
-      const int64_t nlo = f > 0 ? lo + 1 + static_cast<int64_t>(f - 1) * step : lo;
-      hi = pf < hi ? pf : hi;
-      lo = nlo;
-    }
-    if (lane == 0) {
-      start[K] = c;
-      wfirst[K] = wc;
-      const double wl = w[hi - 1];
-      sure[K] = wc > 0.0 ? wl / wc : 1.0;
-    }
+  for (int k = 0; k < kg; ++k) {
+    const int64_t a = bounds[k], b = bounds[k + 1];
+    if (b <= a) continue;
+    if (K >= kmax) { *K_out = -1; return; }
+    start[K] = a;
+    wfirst[K] = w[a];
+    sure[K] = w[b - 1] / w[a];
     ++K;
-    c = hi;
   }
-  if (lane == 0) {
-    start[K] = n;
-    *K_out = (c < n) ? -1 : K;
+  if (z < n) {
+    if (K >= kmax) { *K_out = -1; return; }
+    start[K] = z;
+    wfirst[K] = 0.0;
+    sure[K] = 1.0;
+    ++K;
   }
+  start[K] = n;
+  *K_out = K;
 }
 
 // Hub split plan: for source u in [lo, lo+Hmax) the expected candidate count
