@@ -80,6 +80,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # wait until nvidia-smi is up (its start-up is longer than a short timed
+            # region), then drop that pre-region sample
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
 
@@ -90,6 +96,14 @@ class ClockSampler:
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        at_end = False
+        if not self.lines:
+            # the timed region was shorter than the 200 ms sampling period: take the
+            # first sample after it (GPU just left the region) and say so
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 1.0:
+                time.sleep(0.005)
+            at_end = bool(self.lines)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -111,7 +125,9 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                **({"sampled": "first sample after the timed region (region < 200 ms period)"}
+                   if at_end else {})}
 
 
 def dist_env():
@@ -286,10 +302,10 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
+    clocks.start()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     launches0 = dev.launch_count
     total_ms, kern_ms, edges_total = 0.0, 0.0, 0
     for _ in range(args.steps):
