@@ -140,49 +140,83 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- CPU arm
-def cpu_sample_ranges(w: np.ndarray, target_edges: float, k: int):
-    """k disjoint source ranges, spread evenly over [0,n), each with about
-    target_edges expected edges (suffix-form expected degree, cost.cpp:62-77)."""
-    n = w.size
-    S = float(w.sum())
-    suffix = S - np.cumsum(w)  # sum_{v>u} w_v
-    e = w / S * suffix
-    cum = np.cumsum(e)
-    total = cum[-1]
-    ranges = []
-    for i in range(k):
-        start_cost = total * (i + 0.5) / k
-        lo = int(np.searchsorted(cum, start_cost))
-        hi = int(np.searchsorted(cum, cum[min(lo, n - 1)] + target_edges))
-        hi = max(lo + 1, min(hi, n))
-        ranges.append((lo, hi))
-    return ranges
+def workload_config(name: str, n: int) -> dict:
+    """The workload identity shared by both arms' JSON lines (same `config`)."""
+    import inputs
+    wl = inputs.WORKLOADS[name]
+    return {"workload": f"{name}: {wl.desc}", "n": int(n), "seed": wl.seed,
+            "materialised": wl.materialise}
+
+
+PLAN_PARTS = 64  # plan_ucp_oracle(ws, 64): the sampling frame of SURVEY.md §8(d)
 
 
 class CpuReference:
     """The reference CPU generator (oracle/_ref: the unmodified reference
-    library) on a bounded sample of the workload: `cores` source ranges
-    spread evenly over [0, n), each with about `seconds` of expected work per
-    thread, timed with create_edges_range in parallel std::threads (the
-    acceptance.cpp:221-254 per-partition pattern), count-only sink."""
+    library, compiled from its own sources) on a bounded, extrapolated sample
+    of the workload (SURVEY.md §8(d) "CPU baseline timing"):
+
+    * plan_ucp_oracle(ws, 64) is built once (partition.cpp:159-203);
+    * `cores` of its 64 UCP partitions, evenly spread, are sampled (all 64
+      when the host has >= 64 cores); each contributes the prefix of the
+      partition holding about `seconds` of single-thread work;
+    * create_edges_range runs on those prefixes in parallel std::threads (the
+      acceptance.cpp:221-254 per-partition pattern), count-only EdgeCounter;
+    * value = sampled edges / wall time of the parallel section; the full
+      workload time is extrapolated as m / value.
+    Never imports the product package and never touches the GPU."""
 
     def __init__(self, w: np.ndarray, seconds: float):
         import oracle
         self.cores = os.cpu_count() or 1
         self.R = oracle.ref()
+        t0 = time.time()
         self.ws = self.R.weight_sequence(w)
-        probe = cpu_sample_ranges(w, 2e5, 1)  # ~0.1 s single-range probe: per-thread rate
-        tot, ms = self.R.parallel_ranges_count(self.ws, self.ws.sum_S, probe, 1)
+        S = self.ws.sum_S
+        self.plan = self.R.plan_ucp_oracle(self.ws, PLAN_PARTS)
+        self.plan_s = time.time() - t0
+        # suffix-form expected edges per source (cost.cpp:62-77 minus the 1)
+        # to size each prefix; a sizing aid only, the timing is the reference's
+        cs = np.cumsum(w)
+        e = w / S * (S - cs)
+        ecum = np.cumsum(e)
+        del cs, e
+        self.m = float(ecum[-1])
+        # per-thread rate probe (~0.2 s) at the median partition
+        mid = PLAN_PARTS // 2
+        lo = int(self.plan[mid])
+        hi = self._prefix_end(ecum, lo, int(self.plan[mid + 1]), 1e6)
+        tot, ms = self.R.parallel_ranges_count(self.ws, S, [(lo, hi)], 1)
         rate1 = max(tot / max(ms, 1e-3) * 1e3, 1e5)
-        self.per_thread_edges = rate1 * seconds
-        self.ranges = cpu_sample_ranges(w, self.per_thread_edges, self.cores)
+        self.per_thread = rate1 * seconds
+        k = min(self.cores, PLAN_PARTS)
+        self.parts = sorted({int(round((i + 0.5) * PLAN_PARTS / k - 0.5)) for i in range(k)})
+        self.ranges = []
+        for i in self.parts:
+            lo, end = int(self.plan[i]), int(self.plan[i + 1])
+            self.ranges.append((lo, self._prefix_end(ecum, lo, end, self.per_thread)))
+        self.sample_edges = float(sum(ecum[h - 1] - (ecum[l - 1] if l else 0.0)
+                                      for l, h in self.ranges if h > l))
+        del ecum
+
+    @staticmethod
+    def _prefix_end(ecum, lo, end, edges):
+        base = ecum[lo - 1] if lo else 0.0
+        hi = int(np.searchsorted(ecum, base + edges, side="right")) + 1
+        return max(lo + 1, min(hi, end))
 
     def step(self, seed: int) -> dict:
         tot, ms = self.R.parallel_ranges_count(self.ws, self.ws.sum_S, self.ranges, seed)
-        return {"value": tot / (ms / 1e3), "unit": UNIT, "cores": self.cores, "kind": "reference",
-                "sample": f"{self.cores} source ranges spread over [0,n), "
-                          f"~{self.per_thread_edges:.3g} expected edges each, create_edges_range "
-                          f"in parallel std::threads; {tot} edges in {ms / 1e3:.2f} s"}
+        v = tot / (ms / 1e3)
+        return {"value": v, "unit": UNIT, "cores": len(self.ranges), "kind": "reference",
+                "extrapolated": True, "nproc": self.cores,
+                "sample": (f"prefixes of {len(self.ranges)} of the {PLAN_PARTS} plan_ucp_oracle(ws,"
+                           f"{PLAN_PARTS}) partitions (ids {self.parts[0]}..{self.parts[-1]}), "
+                           f"~{self.per_thread:.3g} expected edges each, create_edges_range in "
+                           f"{len(self.ranges)} parallel std::threads (nproc={self.cores}), "
+                           f"count-only sink: {tot} edges in {ms / 1e3:.2f} s; full workload "
+                           f"m={self.m:.4g} edges extrapolates to {self.m / v:.4g} s"),
+                "plan_s": round(self.plan_s, 1)}
 
 
 def cpu_baseline(w: np.ndarray, seed: int, seconds: float) -> dict:
@@ -190,12 +224,15 @@ def cpu_baseline(w: np.ndarray, seed: int, seconds: float) -> dict:
 
 
 def run_reference(args):
+    """--impl reference: the unmodified reference (oracle/_ref) on the host
+    cores.  Imports only `inputs` (input preparation) and `oracle` (the
+    reference build); under torchrun only rank 0 works."""
     ws_, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_1406_1215_b200 import workloads
-    w = workloads.make(args.config, args.n)
-    seed = workloads.WORKLOADS[args.config].seed
+    import inputs
+    w = inputs.make(args.config, args.n)
+    seed = inputs.WORKLOADS[args.config].seed
     ref = CpuReference(w, args.cpu_seconds / 2)
     vals, step_ms, last = [], [], None
     for i in range(args.warmup + args.steps):
@@ -210,10 +247,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)),
         "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {workloads.WORKLOADS[args.config].desc}",
-                   "n": int(w.size), "step": "one bounded sample of the workload (cpu_baseline.sample)"},
+        "config": workload_config(args.config, w.size),
         "cpu_baseline": {**last, "value": v},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
@@ -254,9 +291,10 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
-    from paper_1406_1215_b200 import api, runtime, workloads
+    import inputs
+    from paper_1406_1215_b200 import api, runtime
 
-    wl = workloads.WORKLOADS[args.config]
+    wl = inputs.WORKLOADS[args.config]
     seed = wl.seed
     t0 = time.time()
     w_host = runtime.shared_weights(args.config, args.n, world, rank, local)
@@ -284,12 +322,16 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     small_inputs = n * 8 < (256 << 20)
 
+    flags = [0]
+
     def step():
         if materialise:
-            e = api.create_edges_range(ws, S, lo, hi, seed, out=out)
+            e, nf = api.create_edges_range(ws, S, lo, hi, seed, out=out, return_flagged=True)
+            flags[0] = max(flags[0], int(nf))
             return int(e.shape[0])
         r = api.stream_range(ws, S, lo, hi, seed, mode=args.mode, track_shift=args.track_shift,
                              degree=deg, accumulate=False, ring=ring)
+        flags[0] = max(flags[0], int(r.flagged))
         return r.count
 
     deg = None
@@ -351,6 +393,9 @@ def run_ours(args):
         dist.all_reduce(e)
         ms_step, kern_step = float(t[0]), float(t[1])
         edges_all = int(e[0]) // args.steps
+        f = torch.tensor([flags[0]], dtype=torch.int64, device=cdev)
+        dist.all_reduce(f)
+        flags[0] = int(f[0])
     else:
         kern_step = kern_ms / args.steps
         edges_all = edges_total // args.steps
@@ -381,7 +426,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {wl.desc}", "n": n, "edges_per_step": edges_all,
+            "config": workload_config(args.config, n),
+            "run": {"edges_per_step": edges_all,
                        "stream_mode": args.mode if not materialise else "reference",
                        "materialised": materialise,
                        "track_shift": None if materialise else args.track_shift,
@@ -399,6 +445,9 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            # sources whose skip ratio fell in the libm-ambiguity band (reference
+            # stream only); the counter stream has none by construction
+            "n_flagged": flags[0],
             "load_balance": {
                 "per_launch_warp_busy": [
                     {"max_over_mean": round(p["max_over_mean"], 4), "mean_ms": round(p["mean_ms"], 3),

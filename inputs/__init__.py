@@ -1,22 +1,46 @@
 """The five BASELINE.json workloads (C1-C5) as seeded synthetic weight arrays.
 
+Input preparation shared by BOTH bench arms and the tests; it is neither the
+product (``paper_1406_1215_b200``, ``libclgen_b200.so``) nor the checker
+(``oracle/``), so the reference arm (``bench.py --impl reference``) never maps
+the product library or touches the GPU.
+
 Recipes follow SURVEY.md §8(d).  Weights are synthesised ONCE on the host by
-the reference's own synthesiser arithmetic (clgen_host_* in the library:
+the reference's own synthesiser arithmetic (``libclgen_inputs.so``: the
 sequential xoshiro synth stream + glibc pow, bit-identical to
-weights.cpp:103-128), so the GPU and the CPU baseline consume identical FP64
-arrays.  Sorting uses a descending sort on the GPU for n >= 1e8 (values only;
-the stable label order of make_weight_sequence does not change them).
+weights.cpp:103-128; tested against the reference's ``synth_powerlaw`` in
+tests/test_oracle.py), then sorted descending on the host with all cores
+(values only; the stable label order of make_weight_sequence does not change
+them).
 """
 from __future__ import annotations
 
 import ctypes as C
 import math
 import os
+import subprocess
+import threading
 from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libclgen_inputs.so")
+_L = None
+_lock = threading.Lock()
+
+
+def build(force: bool = False) -> str:
+    """g++ -O2 (no -march: x86-64 SSE2, no FMA, glibc libm, as the reference build)."""
+    src = os.path.join(HERE, "synth.cpp")
+    hdr = os.path.join(HERE, "clgen_inputs.h")
+    if (not force and os.path.exists(LIB_PATH)
+            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+        return LIB_PATH
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    subprocess.run([cxx, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-shared", "-pthread",
+                    "-o", LIB_PATH, src], check=True)
+    return LIB_PATH
 
 
 @dataclass(frozen=True)
@@ -39,32 +63,37 @@ WORKLOADS = {
 
 
 def _host():
-    L = _lib.lib()
+    global _L
+    with _lock:
+        if _L is None:
+            if not os.path.exists(LIB_PATH):
+                build()
+            L = C.CDLL(LIB_PATH)
+            _declare(L)
+            _L = L
+    return _L
+
+
+def _declare(L):
     L.clgen_host_powerlaw_draws.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double,
                                             C.c_uint64, C.c_void_p, C.c_int]
     L.clgen_host_discrete_powerlaw.argtypes = [C.c_int64, C.c_double, C.c_int64, C.c_int64,
                                                C.c_uint64, C.c_void_p, C.c_int]
     L.clgen_host_sort_desc.argtypes = [C.c_void_p, C.c_int64, C.c_int]
-    return L
 
 
 def _threads() -> int:
     return os.cpu_count() or 1
 
 
-def sort_desc(w: np.ndarray, use_gpu: bool | None = None) -> np.ndarray:
-    """Descending sort of the values (GPU for large arrays, host otherwise)."""
-    if use_gpu is None:
-        use_gpu = w.size >= 50_000_000
-    if use_gpu:
-        import torch
-        t = torch.from_numpy(w).cuda()
-        t = torch.sort(t, descending=True).values
-        out = t.cpu().numpy()
-        del t
-        torch.cuda.empty_cache()
-        return out
-    _lib.check(0 if _host().clgen_host_sort_desc(w.ctypes.data, w.size, _threads()) == 0 else -1)
+class InputError(ValueError):
+    """The reference synthesiser's contract violations (weights.cpp:105-108)."""
+
+
+def sort_desc(w: np.ndarray) -> np.ndarray:
+    """In-place parallel descending sort of the values on the host."""
+    if _host().clgen_host_sort_desc(w.ctypes.data, w.size, _threads()) != 0:
+        raise InputError("sort_desc: bad arguments")
     return w
 
 
@@ -74,7 +103,7 @@ def powerlaw(n: int, gamma: float, w_min: float, w_max: float, seed: int,
     out = np.empty(n, np.float64)
     if _host().clgen_host_powerlaw_draws(n, gamma, w_min, w_max, seed, out.ctypes.data,
                                          _threads()) != 0:
-        raise _lib.error("synth_powerlaw: bad arguments")
+        raise InputError("synth_powerlaw: bad arguments")
     return sort_desc(out) if sort else out
 
 
@@ -82,7 +111,7 @@ def discrete_powerlaw(n: int, gamma: float, k_min: int, k_max: int, seed: int) -
     out = np.empty(n, np.float64)
     if _host().clgen_host_discrete_powerlaw(n, gamma, k_min, k_max, seed, out.ctypes.data,
                                             _threads()) != 0:
-        raise _lib.error("discrete_powerlaw: bad arguments")
+        raise InputError("discrete_powerlaw: bad arguments")
     return sort_desc(out)
 
 

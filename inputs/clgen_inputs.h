@@ -1,13 +1,15 @@
 /*
- * clgen_host.h — host-side input preparation shipped in libclgen_b200.so.
+ * clgen_inputs.h - workload input preparation (libclgen_inputs.so, built by
+ * inputs/__init__.py).  Shared by both bench arms; not part of the product
+ * library, so the reference arm never maps libclgen_b200.so.
  *
  * Not the device hot path: these produce the FP64 weight arrays that both the
  * GPU generator and the CPU baseline consume, bit-identical to the reference
  * synthesisers (weights.cpp:103-140), multi-threaded for n = 1e9.
  * Return 0, or -1 on the reference's contract violations (weights.cpp:105-108).
  */
-#ifndef CLGEN_HOST_H
-#define CLGEN_HOST_H
+#ifndef CLGEN_INPUTS_H
+#define CLGEN_INPUTS_H
 
 #include <stdint.h>
 
@@ -32,4 +34,4 @@ int clgen_host_sort_desc(double* w, int64_t n, int threads);
 }
 #endif
 
-#endif /* CLGEN_HOST_H */
+#endif /* CLGEN_INPUTS_H */

@@ -1,6 +1,7 @@
-// Host-side input preparation (not the device hot path): the reference's
-// weight synthesisers, reproduced bit-for-bit so the GPU and the CPU baseline
-// consume identical FP64 arrays, and parallelised for n = 1e9.
+// libclgen_inputs.so - workload input preparation, shared by both bench arms.
+// It is neither the product (libclgen_b200.so) nor the checker (oracle/): the
+// reference's weight synthesisers, reproduced bit-for-bit so the GPU and the
+// CPU reference consume identical FP64 arrays, parallelised for n = 1e9.
 //
 //   clgen_host_powerlaw_draws  weights.cpp:103-128 (before the descending sort)
 //   clgen_host_discrete_powerlaw  C1 recipe: inverse CDF over
@@ -18,7 +19,7 @@
 #include <thread>
 #include <vector>
 
-#include "../../include/clgen_host.h"
+#include "clgen_inputs.h"
 
 namespace {
 

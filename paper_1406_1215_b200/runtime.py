@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-from . import api, workloads
+from . import api
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -24,26 +24,29 @@ def comm_device(local: int):
 
 
 def shared_weights(config: str, n: int | None, world: int, rank: int, local: int) -> np.ndarray:
-    """Rank 0 synthesises the workload's weights; the other ranks receive them
-    over NCCL (every rank holds all of w)."""
+    """Every rank holds all of w.  Rank 0 synthesises the
+    workload's weights (input preparation, ``inputs``) into a host file that
+    the other ranks map; nothing but a barrier crosses the process group, so
+    the only NCCL traffic of a run stays the plan's scalars."""
+    import inputs
     if world == 1:
-        return workloads.make(config, n)
-    import torch
+        return inputs.make(config, n)
     import torch.distributed as dist
-    dev = comm_device(local)
-    meta = torch.zeros(1, dtype=torch.int64, device=dev)
+    tag = os.environ.get("MASTER_PORT", "0")
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    path = os.path.join(shm, f"clgen_w_{config}_{n or 0}_{tag}.f64")
     w = None
     if rank == 0:
-        w = workloads.make(config, n)
-        meta[0] = w.size
-    dist.broadcast(meta, 0)
-    t = (torch.from_numpy(w).to(dev) if rank == 0
-         else torch.empty(int(meta[0]), dtype=torch.float64, device=dev))
-    dist.broadcast(t, 0)
-    out = t.cpu().numpy() if rank != 0 else w
-    del t
-    torch.cuda.empty_cache()
-    return out
+        w = inputs.make(config, n)
+        w.tofile(path + ".part")
+        os.replace(path + ".part", path)
+    dist.barrier()
+    if rank != 0:
+        w = np.fromfile(path, dtype=np.float64)
+    dist.barrier()
+    if rank == 0:
+        os.remove(path)
+    return w
 
 
 def plan(ws: api.WeightSequence, world: int, rank: int) -> np.ndarray:

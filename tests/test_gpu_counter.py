@@ -89,7 +89,7 @@ def test_pair_frequencies_match_law(api):
 @pytest.mark.parametrize("name,n,eps", [("c3", 1_000_000, 0.125), ("c5", 1_000_000, 0.125),
                                         ("c3", 1_000_000, 0.5)])
 def test_degree_chi2(api, name, n, eps):
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.make(name, n)
     ws = api.make_weight_sequence(w)
     ws.device.set_counter_params(class_eps=eps, split_cap=1024.0)
@@ -121,7 +121,7 @@ def test_heavy_light_split_and_law(api, port):
     """Both kernels (warp-cooperative heavy units, lane-per-unit light units)
     run and the joint output keeps the law; heavy/light choice per source is
     a function of the weights only, so partitions agree."""
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.make("c4", 400_000)
     ws = api.make_weight_sequence(w)
     full = api.stream_range(ws, ws.sum_S, 0, w.size, 99, mode="counter", track_shift=0)
@@ -145,7 +145,7 @@ def test_kernel_shape_invariance(api, name, n):
     block shape of the heavy-unit kernel (2-4 resident 256-thread blocks,
     128-thread blocks) and the forward-walk class lookup give the same edge
     count, checksum and tracked degrees, and the materialised pass matches."""
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.make(name, n)
     ws = api.make_weight_sequence(w)
     base = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)

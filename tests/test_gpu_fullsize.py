@@ -25,7 +25,7 @@ def api():
 
 @pytest.fixture(scope="module")
 def c4(api):
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.make("c4")
     return w, api.make_weight_sequence(w)
 

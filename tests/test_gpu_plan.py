@@ -77,7 +77,7 @@ def test_random_plans_vs_oracle(api, port):
 
 def test_c1_plans_match_reference(api):
     s = json.load(open(os.path.join(GOLDEN, "scalars.json")))["c1_continuous"]
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.powerlaw(1_000_000, 2.5, 10.0, 1000.0, 1)
     ws = api.make_weight_sequence(w)
     for P in (2, 4, 8):
@@ -86,7 +86,7 @@ def test_c1_plans_match_reference(api):
 
 def test_large_fold_many_binades(api, port):
     # a 20M-element fold crossing many binades, spine + emit on thousands of tiles
-    from paper_1406_1215_b200 import workloads
+    import inputs as workloads
     w = workloads.make("c3", 20_000_000)
     ws = api.make_weight_sequence(w)
     for P in (1, 8):

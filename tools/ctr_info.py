@@ -2,7 +2,8 @@
 import sys, time
 sys.path.insert(0, '.')
 import torch
-from paper_1406_1215_b200 import api, workloads
+from paper_1406_1215_b200 import api
+import inputs as workloads
 name = sys.argv[1]; n = int(float(sys.argv[2])) if len(sys.argv) > 2 else None
 w = workloads.make(name, n)
 ws = api.make_weight_sequence(w)

@@ -1,7 +1,8 @@
 """Time the reference-stream fold on a workload (kernel ms)."""
 import sys, time
 sys.path.insert(0, '.')
-from paper_1406_1215_b200 import api, workloads
+from paper_1406_1215_b200 import api
+import inputs as workloads
 name = sys.argv[1]; n = int(float(sys.argv[2])) if len(sys.argv) > 2 else None
 mode = sys.argv[3] if len(sys.argv) > 3 else "reference"
 w = workloads.make(name, n)
