@@ -35,7 +35,8 @@ typedef struct clgen_dev_ctx clgen_dev_ctx;
 
 /* Stream modes for the sampler. */
 #define CLGEN_STREAM_REFERENCE 0 /* per-node xoshiro256++ (rng.hpp:26-69): bit-exact */
-#define CLGEN_STREAM_COUNTER 1   /* keyed xoshiro256+ per (seed,u,split,lane): statistical, GPU-count invariant */
+#define CLGEN_STREAM_COUNTER 1   /* keyed xoroshiro128++ per (seed,class-pair block,chunk,lane):
+                                    statistical, GPU-count / partition / launch invariant */
 
 const char* clgen_dev_last_error(void);
 const char* clgen_dev_version(void);
@@ -107,10 +108,11 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
                              int64_t* n_flagged);
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
- * w_last inside a class; default 1/128, doubled until at most 1024 classes) and the hub split size in expected
- * candidates (0 = automatic, the default: S / 2^17 clamped to [1024, 8192],
- * a function of the weights only).  Changing them changes the generated graph. */
-int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double split_cap);
+ * w_last inside a class; default 1/128, doubled until the classes fit 1024)
+ * and the chunk size in expected candidates (0 = default 32768; range
+ * [256, 2^20]).  Both are part of the stream definition: changing them
+ * changes the generated graph (not its law). */
+int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double chunk_cand);
 /* Reference stream arithmetic: 1 (default) = fast guarded FP64 (table log,
  * series log1p, FMA-certified divisions; falls back to the reference
  * expressions near rounding/floor boundaries, so results are identical);
@@ -118,26 +120,24 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double sp
 int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
 /* Level-2 load-balance evidence: when enabled, the sampler kernels record
  * each warp's busy interval (%globaltimer).  For sampler launch `launch` of
- * the last generation call (0 .. clgen_dev_warp_profile_launches()-1; the
- * counter stream runs a heavy-unit and a light-unit kernel) report max/mean
+ * the last generation call (0 .. clgen_dev_warp_profile_launches()-1) report max/mean
  * per-warp busy time, mean and max in ms, the span first-start to last-end,
  * and the number of warps. */
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
 
 /* Counter-stream kernel shape (no reference counterpart; the edge set does
- * not depend on it): warp_cfg selects the heavy-unit kernel's block shape
- * (0 = 256 threads x 2 blocks/SM, 1 = 256x3, 2 = 256x4 (default), 3 = 128x6,
- * 4 = 128x7, 5 = 128x8, -1 = CLGEN_WARP_CFG or the default); deep_lookup != 0
- * forces the forward-walk class lookup instead of the two-compare bucket
- * lookup.  Used by the schedule-invariance tests. */
-int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int warp_cfg, int deep_lookup);
+ * not depend on it): 0 = 256 threads x 2 CTAs/SM, 1 = 256x3, 2 = 256x4
+ * (default), 3 = 128x8, -1 = CLGEN_BLK_SHAPE or the default.  flags must be
+ * 0.  Used by the schedule-invariance tests. */
+int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int shape, int flags);
 int clgen_dev_warp_profile_launches(clgen_dev_ctx* ctx);
 int clgen_dev_warp_profile(clgen_dev_ctx* ctx, int launch, double* max_over_mean, double* mean_ms,
                            double* max_ms, double* span_ms, int64_t* warps);
-/* Size of the last counter plan: weight classes, split sources, work units;
- * and how many units (a prefix) run on the warp-cooperative kernel. */
-int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* hubs, int64_t* units);
-int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* ctx);
+/* Size of the counter plan of the last counter-stream call: weight classes
+ * (incl. the zero class), class-pair blocks, chunks over all sources, dense
+ * blocks (envelope >= 1) and the class width actually used. */
+int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* blocks, int64_t* chunks,
+                                int* dense_blocks, double* class_eps);
 
 /* Count pass only: per-source edge counts (int32, hi-lo entries, host or device). */
 int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,

@@ -80,9 +80,8 @@ def _declare(L):
     L.clgen_dev_set_kernel_shape.argtypes = [_vp, C.c_int, C.c_int]
     L.clgen_dev_warp_profile.argtypes = [_vp, C.c_int, _dp, _dp, _dp, _dp, _i64p]
     L.clgen_dev_warp_profile_launches.argtypes = [_vp]
-    L.clgen_dev_counter_heavy_units.restype = _i64
-    L.clgen_dev_counter_heavy_units.argtypes = [_vp]
-    L.clgen_dev_counter_plan_info.argtypes = [_vp, C.POINTER(C.c_int), _i64p, _i64p]
+    L.clgen_dev_counter_plan_info.argtypes = [_vp, C.POINTER(C.c_int), _i64p, _i64p,
+                                              C.POINTER(C.c_int), _dp]
     L.clgen_dev_plan_ucp.argtypes = [_vp, C.c_int, _vp, _vp]
     L.clgen_dev_plan_block_weight.argtypes = [_vp, C.c_int, C.c_int, _dp]
     L.clgen_dev_plan_block_costs.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, _dp]
@@ -101,7 +100,7 @@ EXPORTS = (
     "clgen_dev_flagged_nodes", "clgen_dev_plan_ucp", "clgen_dev_plan_block_weight",
     "clgen_dev_plan_block_costs", "clgen_dev_plan_block_boundaries", "clgen_dev_generate_range",
     "clgen_dev_set_counter_params", "clgen_dev_counter_plan_info", "clgen_dev_set_fast_math",
-    "clgen_dev_counter_heavy_units", "clgen_dev_set_warp_profile", "clgen_dev_set_kernel_shape", "clgen_dev_warp_profile",
+"clgen_dev_set_warp_profile", "clgen_dev_set_kernel_shape", "clgen_dev_warp_profile",
     "clgen_dev_warp_profile_launches", "clgen_dev_write_edges",
     "clgen_dev_fidelity", "clgen_dev_edge_degrees",
 )

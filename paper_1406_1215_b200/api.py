@@ -136,19 +136,21 @@ class Device:
         check(_lib.lib().clgen_dev_blocked_sum(self._h, C.byref(out)))
         return out.value
 
-    def set_counter_params(self, class_eps: float = 1.0 / 128, split_cap: float = 0.0) -> None:
-        """Counter-stream weight-class width and hub split size (changes the graph)."""
-        check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, split_cap))
+    def set_counter_params(self, class_eps: float = 1.0 / 128, chunk_cand: float = 0.0) -> None:
+        """Counter-stream weight-class width and chunk size in expected
+        candidates (0: default); part of the stream definition (changes the
+        graph, not its law)."""
+        check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, chunk_cand))
 
     def set_fast_math(self, enable: bool = True) -> None:
         """Reference-stream arithmetic: guarded fast path (default) or the
         reference expressions everywhere; both give identical edges."""
         check(_lib.lib().clgen_dev_set_fast_math(self._h, int(bool(enable))))
 
-    def set_kernel_shape(self, warp_cfg: int = -1, deep_lookup: bool = False) -> None:
-        """Counter-stream kernel shape (block shape of the heavy-unit kernel,
-        forward-walk class lookup); the edge set does not depend on it."""
-        check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(warp_cfg), int(bool(deep_lookup))))
+    def set_kernel_shape(self, shape: int = -1) -> None:
+        """Counter-stream kernel block shape (0: 256x2, 1: 256x3, 2: 256x4,
+        3: 128x8 threads x CTAs/SM; -1 default); the edge set does not depend on it."""
+        check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(shape), 0))
 
     def set_warp_profile(self, enable: bool = True) -> None:
         check(_lib.lib().clgen_dev_set_warp_profile(self._h, int(bool(enable))))
@@ -168,10 +170,13 @@ class Device:
         return out
 
     def counter_plan_info(self) -> dict:
-        k, h, u = C.c_int(), C.c_int64(), C.c_int64()
-        check(_lib.lib().clgen_dev_counter_plan_info(self._h, C.byref(k), C.byref(h), C.byref(u)))
-        return {"classes": k.value, "hubs": h.value, "units": u.value,
-                "heavy_units": int(_lib.lib().clgen_dev_counter_heavy_units(self._h))}
+        """Counter plan of the last counter-stream call: classes, class-pair
+        blocks, chunks over all sources, dense blocks, class width used."""
+        k, b, ch, dn, eps = C.c_int(), C.c_int64(), C.c_int64(), C.c_int(), C.c_double()
+        check(_lib.lib().clgen_dev_counter_plan_info(self._h, C.byref(k), C.byref(b), C.byref(ch),
+                                                     C.byref(dn), C.byref(eps)))
+        return {"classes": k.value, "blocks": b.value, "chunks": ch.value,
+                "dense_blocks": dn.value, "class_eps": eps.value}
 
     def flagged_nodes(self) -> np.ndarray:
         n = C.c_int64()

@@ -6,6 +6,7 @@
 // result must be returned to the caller.
 
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <cstdarg>
 #include <cstdlib>
@@ -22,7 +23,7 @@
 #include "plan.cuh"
 #include "edge_io.cuh"
 #include "fidelity.cuh"
-#include "sampler_ctr.cuh"
+#include "sampler_blk.cuh"
 #include "sampler_ref.cuh"
 #include "scan.cuh"
 #include "weights.cuh"
@@ -130,29 +131,22 @@ struct clgen_dev_ctx {
   bool one_pass = env_double("CLGEN_REF_1PASS", 1.0) != 0.0;
   double slot_sigma = env_double("CLGEN_REF_SLOT_SIGMA", 6.0), slot_const = env_double("CLGEN_REF_SLOT_CONST", 8.0);
   int plan_G = 0;  // blocks of the cost profile currently held in `cum`
-  // counter stream: weight-class segment table (per weights) and the hub
-  // split plan of the last source range
-  DevBuf grid_thr, grid_bounds;  // class grid thresholds / boundaries (ensure_segments)
-  DevBuf seg_start, seg_wfirst, seg_sure, seg_mass, seg_em, seg_invwf, seg_bucket, hub_units, split_pos, unit_counts;
-  int seg_K = 0;
-  int seg_depth = 64;  // bucket lookup depth (segment_buckets_kernel)
-  int seg_nb = clg::kBuckets;  // buckets in the class index
-  double seg_em_end = 0.0;     // envelope mass em[K]
-  double seg_eps_used = 0.0;   // class width after doubling to fit the cap
-  bool seg_valid = false;
-  double seg_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
-  double split_cap = env_double("CLGEN_CTR_SPLIT", 0.0);  // 0: auto (effective_split_cap)
-  int64_t ctr_lo = -1, ctr_hi = -1, ctr_H = 0, ctr_units = 0, ctr_heavy = 0;
-  double ctr_S = 0.0;  // S the cached hub plan was built for
-  double heavy_cand = env_double("CLGEN_CTR_HEAVY", 384.0);  // units with >= this many expected candidates run warp-cooperatively
-  DevBuf probe;
-  int ctr_blocks[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-  int ctr_warp_blocks[3] = {0, 0, 0};
-  size_t ctr_warp_smem[3] = {0, 0, 0};
-  size_t ctr_walk_smem[3][3] = {};
-  int ctr_warp_cfg[3] = {-1, -1, -1};
-  int warp_cfg = -1;       // clgen_dev_set_kernel_shape (-1: CLGEN_WARP_CFG / default)
-  bool force_deep = false;  // class lookup by forward walk (test hook)
+  // counter stream (sampler_blk.cuh): class table per weights, block table
+  // per (weights, S), chunk tables per launch range
+  DevBuf cls_thr, cls_bounds, cls_start, cls_wfirst, cls_wlast, cls_plan;
+  DevBuf blocks, ranges, blk_cnt, blk_prefix, chunk_block, chunk_total, chunk_counts, chunk_offsets;
+  DevBuf keys_a, keys_b, sort_tmp;  // materialised counter output: device sort by (u, v)
+  DevBuf probe;                     // small scratch (fidelity histograms)
+  clg::ClassPlan plan_host{};
+  bool cls_valid = false;
+  bool blk_valid = false;
+  double blk_S = 0.0;
+  int64_t rng_lo = -1, rng_hi = -1;  // launch range the chunk tables hold
+  double cls_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
+  double chunk_cand = env_double("CLGEN_CTR_CHUNK", 32768.0);
+  int blk_shape = -1;  // clgen_dev_set_kernel_shape (-1: CLGEN_BLK_SHAPE / default)
+  int blk_grid[3][4] = {};
+  size_t blk_smem[3][4] = {};
   // optional per-warp busy intervals of the sampler kernels
   bool warp_prof = false;
   DevBuf prof;
@@ -164,7 +158,6 @@ struct clgen_dev_ctx {
   int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
-  int ctr_refill_min = static_cast<int>(env_double("CLGEN_CTR_REFILL_MIN", 4.0));
   clg::LogTable* logtab = nullptr;  // device
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
@@ -434,370 +427,225 @@ int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, doubl
   return CLGEN_OK;
 }
 
-// ---- counter stream (sampler_ctr.cuh) ----------------------------------------
-clg::Segments segments(clgen_dev_ctx* c);
-
-int ensure_segments(clgen_dev_ctx* c) {
-  if (c->seg_valid) return CLGEN_OK;
-  const int kmax = clg::kSegSmemMax;
-  CUDA_TRY(c->seg_start.ensure((kmax + 1) * sizeof(int64_t)));
-  CUDA_TRY(c->seg_wfirst.ensure((kmax + 1) * sizeof(double)));
-  CUDA_TRY(c->seg_sure.ensure((kmax + 1) * sizeof(double)));
-  CUDA_TRY(c->seg_mass.ensure((kmax + 1) * sizeof(double)));
-  CUDA_TRY(c->seg_em.ensure((kmax + 1) * sizeof(double)));
-  CUDA_TRY(c->seg_invwf.ensure((kmax + 1) * sizeof(double)));
-  CUDA_TRY(c->seg_bucket.ensure(clg::kBuckets * sizeof(unsigned short)));
-  // zero weights start at z; the positive range is [w[z-1], w[0]]
-  double tiny;  // smallest positive double: w < tiny <=> w == 0 for non-negative weights
-  {
-    const long long one = 1;
-    std::memcpy(&tiny, &one, sizeof tiny);
-  }
-  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, 0, c->n, tiny,
-                                                   reinterpret_cast<long long*>(&c->sc->total));
-  ++c->launches;
-  CUDA_TRY(cudaGetLastError());
-  long long z = 0;
-  CUDA_TRY(cudaMemcpyAsync(&z, &c->sc->total, sizeof z, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  double wmax = 0.0, wmin = 0.0;
-  if (z > 0) {
-    CUDA_TRY(cudaMemcpy(&wmax, c->w, sizeof(double), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(&wmin, c->w + (z - 1), sizeof(double), cudaMemcpyDeviceToHost));
-  }
-  // grid width: the requested eps, doubled until the grid fits the class cap
-  double eps = c->seg_eps;
-  const int zero_class = z < c->n ? 1 : 0;
-  int kg = 0;
-  for (int attempt = 0; attempt < 40; ++attempt, eps *= 2.0) {
-    const double cells = z > 0 ? std::ceil(std::log(wmax / wmin) / std::log1p(eps)) + 1.0 : 0.0;
-    if (cells + zero_class <= kmax) {
-      kg = static_cast<int>(cells);
-      break;
-    }
-  }
-  if (z > 0 && kg == 0) return fail(CLGEN_EINVAL, "counter stream: weight range too wide for the class table");
-  {
-    std::vector<double> thr(kg + 1, 0.0);
-    double t = wmax;
-    for (int k = 1; k < kg; ++k) thr[k] = (t = t / (1.0 + eps));
-    CUDA_TRY(c->grid_thr.ensure((kg + 2) * sizeof(double)));
-    CUDA_TRY(c->grid_bounds.ensure((kg + 2) * sizeof(int64_t)));
-    CUDA_TRY(cudaMemcpyAsync(c->grid_thr.p, thr.data(), (kg + 1) * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    clg::grid_bounds_kernel<<<(kg + 1 + 255) / 256, 256, 0, c->stream>>>(c->w, z, c->grid_thr.as<double>(), kg,
-                                                                        c->grid_bounds.as<int64_t>());
-    clg::grid_compact_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, z, c->grid_bounds.as<int64_t>(), kg, kmax,
-                                                     c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(),
-                                                     c->seg_sure.as<double>(), reinterpret_cast<int*>(&c->sc->total));
-    c->launches += 2;
+// ---- counter stream (sampler_blk.cuh) ----------------------------------------
+// Class table of the weights (no host round trip) and block table for S (one
+// synchronisation: the host learns the class and chunk counts to size the
+// per-launch tables); both cached until the weights, S or the parameters change.
+int ensure_blocks(clgen_dev_ctx* c, double S) {
+  if (c->blk_valid && c->blk_S == S) return CLGEN_OK;
+  const int kcap = clg::kClassCap;
+  if (!c->cls_valid) {
+    CUDA_TRY(c->cls_thr.ensure((kcap + 2) * sizeof(double)));
+    CUDA_TRY(c->cls_bounds.ensure((kcap + 2) * sizeof(int64_t)));
+    CUDA_TRY(c->cls_start.ensure((kcap + 2) * sizeof(int64_t)));
+    CUDA_TRY(c->cls_wfirst.ensure((kcap + 1) * sizeof(double)));
+    CUDA_TRY(c->cls_wlast.ensure((kcap + 1) * sizeof(double)));
+    CUDA_TRY(c->cls_plan.ensure(sizeof(clg::ClassPlan)));
+    CUDA_TRY(cudaMemsetAsync(c->cls_plan.p, 0, sizeof(clg::ClassPlan), c->stream));
+    clg::ClassPlan* dp = c->cls_plan.as<clg::ClassPlan>();
+    clg::cls_grid_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, c->cls_eps, kcap, c->cls_thr.as<double>(), dp);
+    clg::cls_bounds_kernel<<<(kcap + 256) / 256, 256, 0, c->stream>>>(c->w, c->cls_thr.as<double>(), dp, kcap,
+                                                                        c->cls_bounds.as<int64_t>());
+    clg::cls_compact_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, c->cls_bounds.as<int64_t>(), kcap, dp,
+                                                    c->cls_start.as<int64_t>(), c->cls_wfirst.as<double>(),
+                                                    c->cls_wlast.as<double>());
+    c->launches += 3;
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaStreamSynchronize(c->stream));  // thr is a host vector
   }
+  clg::ClassPlan* dp = c->cls_plan.as<clg::ClassPlan>();
+  CUDA_TRY(cudaMemsetAsync(&dp->chunks_full, 0, sizeof(unsigned long long), c->stream));
+  CUDA_TRY(cudaMemsetAsync(&dp->dense_blocks, 0, sizeof(int), c->stream));
+  const int64_t nb_max = static_cast<int64_t>(kcap) * (kcap + 1) / 2;
+  CUDA_TRY(c->blocks.ensure(nb_max * sizeof(clg::BlockDesc)));
   {
-    int K = 0;
-    CUDA_TRY(cudaMemcpyAsync(&K, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    c->seg_eps_used = eps;
-    if (K > 0) {
-      c->seg_K = K;
-      clg::Segments sg = segments(c);
-      sg.K = K;
-      clg::segment_envelope_kernel<<<1, 32, 0, c->stream>>>(sg, c->seg_em.as<double>(), c->seg_invwf.as<double>(),
-                                                            c->seg_mass.as<double>());
-      // smallest bucket index (4096, then 8192) whose lookups need <= 2 steps
-      int depth = 0;
-      for (int nb = 4096; nb <= clg::kBuckets; nb *= 2) {
-        sg.nb = nb;
-        CUDA_TRY(cudaMemsetAsync(&c->sc->total, 0, sizeof(int64_t), c->stream));
-        clg::segment_buckets_kernel<<<(nb + 255) / 256, 256, 0, c->stream>>>(
-            sg, c->seg_bucket.as<unsigned short>(), reinterpret_cast<int*>(&c->sc->total));
-        ++c->launches;
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaMemcpyAsync(&depth, &c->sc->total, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
-        c->seg_nb = nb;
-        if (depth <= 2) break;
-      }
-      ++c->launches;  // segment_envelope_kernel
-      c->seg_depth = depth;
-      CUDA_TRY(cudaMemcpy(&c->seg_em_end, c->seg_em.as<double>() + K, sizeof(double), cudaMemcpyDeviceToHost));
-      c->seg_valid = true;
-      return CLGEN_OK;
-    }
-  }
-  return fail(CLGEN_EINVAL, "counter stream: weight range too wide for the class table");
-}
-
-clg::Segments segments(clgen_dev_ctx* c) {
-  return clg::Segments{c->seg_start.as<int64_t>(), c->seg_wfirst.as<double>(), c->seg_sure.as<double>(),
-                       c->seg_em.as<double>(), c->seg_invwf.as<double>(), c->seg_K,
-                       c->seg_bucket.as<unsigned short>(), c->force_deep ? 64 : c->seg_depth, c->seg_nb, c->seg_em_end,
-                       static_cast<double>(c->seg_nb) / c->seg_em_end};
-}
-
-// Hub split plan for sources [lo,hi): sources whose envelope-expected
-// candidate count exceeds split_cap are split into v-ranges of ~split_cap.
-// The automatic cap is a function of the weights only (S, so every rank and
-// every partition of the sources uses the same plan): S/2 bounds the expected
-// edge count, and splits of 1/2^16 of it, clamped to [1024, 8192] expected
-// candidates, keep small graphs balanced and large ones cheap per unit.
-double effective_split_cap(const clgen_dev_ctx* c, double S) {
-  if (c->split_cap > 0.0) return c->split_cap;
-  const double cap = S / 131072.0;
-  return cap < 1024.0 ? 1024.0 : (cap > 8192.0 ? 8192.0 : cap);
-}
-
-int ensure_ctr_plan(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi) {
-  int rc = ensure_segments(c);
-  if (rc) return rc;
-  if (c->ctr_lo == lo && c->ctr_hi == hi && c->ctr_S == S) return CLGEN_OK;
-  // E_u <= w_u (1+eps): only sources with w_u >= cap/(1+eps) can be hubs
-  const double split_cap = effective_split_cap(c, S);
-  clg::first_below_kernel<<<1, 32, 0, c->stream>>>(c->w, lo, hi, split_cap / (1.0 + 2.0 * c->seg_eps),
-                                                   reinterpret_cast<long long*>(&c->sc->total));
-  ++c->launches;
-  CUDA_TRY(cudaGetLastError());
-  long long fb = 0;
-  CUDA_TRY(cudaMemcpyAsync(&fb, &c->sc->total, sizeof fb, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  const int64_t H = fb - lo;
-  c->ctr_H = H;
-  int64_t hub_total = 0;
-  if (H > 0) {
-    CUDA_TRY(c->hub_units.ensure((H + 1) * sizeof(int64_t)));
-    CUDA_TRY(c->counts.ensure(H * sizeof(int64_t)));  // scratch: per-hub split counts
-    int64_t* splits = reinterpret_cast<int64_t*>(c->counts.p);
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((H + 255) / 256, c->num_sms * 8));
-    clg::hub_splits_kernel<<<grid, 256, 0, c->stream>>>(c->w, c->n, S, lo, H, segments(c), c->seg_mass.as<double>(),
-                                                      split_cap, splits);
+    const dim3 blk(32, 8), grd((kcap + 31) / 32, (kcap + 7) / 8);
+    clg::blk_desc_kernel<<<grd, blk, 0, c->stream>>>(c->cls_start.as<int64_t>(), c->cls_wfirst.as<double>(),
+                                                     c->cls_wlast.as<double>(), dp, S, c->chunk_cand,
+                                                     c->blocks.as<clg::BlockDesc>());
     ++c->launches;
     CUDA_TRY(cudaGetLastError());
-    // exclusive scan of split counts -> hub_units[0..H), total -> hub_units[H]
-    const int64_t ntiles = (H + clg::kScanTile - 1) / clg::kScanTile;
+  }
+  CUDA_TRY(cudaMemcpyAsync(&c->plan_host, dp, sizeof(clg::ClassPlan), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->plan_host.K < 0) return fail(CLGEN_EINVAL, "counter stream: weight range too wide for the class table");
+  c->plan_host.nblocks = static_cast<int64_t>(c->plan_host.Knz) * (c->plan_host.Knz + 1) / 2;
+  c->cls_valid = true;
+  c->blk_valid = true;
+  c->blk_S = S;
+  c->rng_lo = c->rng_hi = -1;
+  return CLGEN_OK;
+}
+
+// Per launch range [lo, hi): chunks per block, their prefix (total on the
+// device) and the chunk -> block map.  No host round trip.
+int ensure_range(clgen_dev_ctx* c, int64_t lo, int64_t hi) {
+  if (c->rng_lo == lo && c->rng_hi == hi) return CLGEN_OK;
+  const int64_t nb = c->plan_host.nblocks;
+  const int64_t cf = static_cast<int64_t>(c->plan_host.chunks_full);
+  CUDA_TRY(c->ranges.ensure((nb > 0 ? nb : 1) * sizeof(clg::BlockRange)));
+  CUDA_TRY(c->blk_cnt.ensure((nb > 0 ? nb : 1) * sizeof(int64_t)));
+  CUDA_TRY(c->blk_prefix.ensure((nb > 0 ? nb : 1) * sizeof(int64_t)));
+  CUDA_TRY(c->chunk_block.ensure((cf > 0 ? cf : 1) * sizeof(uint32_t)));
+  CUDA_TRY(c->chunk_total.ensure(sizeof(int64_t)));
+  CUDA_TRY(cudaMemsetAsync(c->chunk_total.p, 0, sizeof(int64_t), c->stream));
+  if (nb > 0) {
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + 255) / 256, c->num_sms * 8));
+    clg::blk_range_kernel<<<grid, 256, 0, c->stream>>>(c->blocks.as<clg::BlockDesc>(), nb, lo, hi,
+                                                       c->ranges.as<clg::BlockRange>(), c->blk_cnt.as<int64_t>());
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    const int64_t ntiles = (nb + clg::kScanTile - 1) / clg::kScanTile;
     CUDA_TRY(c->tiles.ensure(ntiles * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(c->tiles.p, 0, ntiles * sizeof(unsigned long long), c->stream));
     CUDA_TRY(cudaMemsetAsync(&c->sc->ticket, 0, sizeof(unsigned long long), c->stream));
     clg::scan_lookback_kernel<int64_t><<<static_cast<unsigned>(ntiles), clg::kScanThreads, 0, c->stream>>>(
-        splits, c->hub_units.as<int64_t>(), H, c->tiles.as<unsigned long long>(), &c->sc->ticket,
-        c->hub_units.as<int64_t>() + H, 0);
-    ++c->launches;
+        c->blk_cnt.as<int64_t>(), c->blk_prefix.as<int64_t>(), nb, c->tiles.as<unsigned long long>(), &c->sc->ticket,
+        c->chunk_total.as<int64_t>(), 0);
+    const unsigned mgrid = static_cast<unsigned>(std::min<int64_t>((nb + 7) / 8, c->num_sms * 16));
+    clg::blk_chunk_map_kernel<<<mgrid, 256, 0, c->stream>>>(c->blk_cnt.as<int64_t>(), c->blk_prefix.as<int64_t>(), nb,
+                                                            c->chunk_block.as<uint32_t>());
+    c->launches += 2;
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(&hub_total, c->hub_units.as<int64_t>() + H, sizeof hub_total, cudaMemcpyDeviceToHost,
-                             c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    CUDA_TRY(c->split_pos.ensure((hub_total + 1) * sizeof(int64_t)));
-    clg::hub_positions_kernel<<<grid, 256, 0, c->stream>>>(c->w, c->n, S, lo, H, segments(c), c->seg_mass.as<double>(),
-                                                         c->hub_units.as<int64_t>(), c->split_pos.as<int64_t>());
-    ++c->launches;
-    CUDA_TRY(cudaGetLastError());
-  } else {
-    CUDA_TRY(c->hub_units.ensure(sizeof(int64_t)));
-    CUDA_TRY(c->split_pos.ensure(sizeof(int64_t)));
   }
-  c->ctr_units = hub_total + (hi - lo - (H > 0 ? H : 0));
-  // heavy plain sources: a prefix of [lo+H, hi) with expected candidates >=
-  // heavy_cand (the estimate is non-increasing in u); bracketed by sampling
-  // up to 1024 points per pass
-  {
-    const int64_t a0 = lo + (H > 0 ? H : 0);
-    int64_t lo_b = a0, hi_b = hi;  // answer (first light source) in [lo_b, hi_b]
-    const int mmax = 1024;
-    CUDA_TRY(c->probe.ensure(mmax * sizeof(double)));
-    std::vector<double> e(mmax);
-    while (hi_b > lo_b) {
-      const int64_t span = hi_b - lo_b;
-      const int m = static_cast<int>(span < mmax ? span : mmax);
-      clg::expected_candidates_kernel<<<(m + 255) / 256, 256, 0, c->stream>>>(
-          c->w, c->n, S, segments(c), c->seg_mass.as<double>(), lo_b, hi_b, m, c->probe.as<double>());
-      ++c->launches;
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaMemcpyAsync(e.data(), c->probe.p, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_TRY(cudaStreamSynchronize(c->stream));
-      int i = 0;
-      while (i < m && e[i] >= c->heavy_cand) ++i;
-      auto ui = [&](int t) { return lo_b + span * t / m; };
-      if (i == m) {
-        lo_b = ui(m - 1) + 1;
-      } else if (i == 0) {
-        hi_b = lo_b;
-      } else {
-        const int64_t na = ui(i - 1) + 1, nb = ui(i);
-        lo_b = na;
-        hi_b = nb;
-      }
-    }
-    // light units must be plain pure-hazard sources (no pbar >= 1/16 band):
-    // the band screen is monotone in u, so those form a suffix
-    clg::first_pure_hazard_kernel<<<1, 32, 0, c->stream>>>(c->w, c->n, a0, hi, 1.0 / S,
-                                                           reinterpret_cast<long long*>(&c->sc->total));
-    ++c->launches;
-    CUDA_TRY(cudaGetLastError());
-    long long pure0 = hi;
-    CUDA_TRY(cudaMemcpyAsync(&pure0, &c->sc->total, sizeof pure0, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    c->ctr_heavy = hub_total + (std::max<int64_t>(lo_b, pure0) - a0);
-  }
-  c->ctr_lo = lo;
-  c->ctr_S = S;
-  c->ctr_hi = hi;
+  c->rng_lo = lo;
+  c->rng_hi = hi;
   return CLGEN_OK;
 }
 
-clg::CtrWalkArgs ctr_args(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed) {
-  clg::CtrWalkArgs a;
+clg::BlkArgs blk_args(clgen_dev_ctx* c, double S, uint64_t seed) {
+  clg::BlkArgs a;
   std::memset(&a, 0, sizeof a);
   a.w = c->w;
-  a.n = c->n;
   a.S = S;
-  a.invS = 1.0 / S;
-  a.lo = lo;
-  a.hi = hi;
-  c->seed_mix = clg::mix64(seed ^ 0x636c67656e637472ULL);  // "clgenctr" domain tag
-  a.refill_min = c->ctr_refill_min;
-  a.seg = segments(c);
-  a.H = c->ctr_H;
-  a.hub_units = c->hub_units.as<int64_t>();
-  a.total_units = c->ctr_units;
+  a.blocks = c->blocks.as<clg::BlockDesc>();
+  a.ranges = c->ranges.as<clg::BlockRange>();
+  a.chunk_prefix = c->blk_prefix.as<int64_t>();
+  a.chunk_block = c->chunk_block.as<uint32_t>();
+  a.total_chunks = c->chunk_total.as<int64_t>();
   a.queue = &c->sc->queue;
+  a.seed_mix = clg::mix64(seed ^ 0x636c67656e626c6bULL);  // "clgenblk" domain tag
+  a.logtab = c->logtab;
   a.overflow = &c->sc->overflow;
   a.fold_out = c->sc->fold;
   return a;
 }
 
-template <int MODE, int MINB>
-int launch_ctr_lane(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in, int slot) {
-  clg::CtrWalkArgs a = a_in;
-  const size_t smem = clg::ctr_walk_smem_bytes(c->seg_K, c->seg_nb);
-  if (!c->ctr_blocks[slot][MODE] || c->ctr_walk_smem[slot][MODE] != smem) {
-    if (smem > 48 * 1024)
-      CUDA_TRY(cudaFuncSetAttribute(clg::ctr_walk_kernel<MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ctr_walk_kernel<MODE, MINB>, 256, smem));
-    c->ctr_blocks[slot][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
-    c->ctr_walk_smem[slot][MODE] = smem;
-  }
-  a.prof = prof_slots(c, c->ctr_blocks[slot][MODE], c->ctr_heavy == 0);
-  clg::ctr_walk_kernel<MODE, MINB><<<c->ctr_blocks[slot][MODE], 256, smem, c->stream>>>(
-      a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix);
-  CUDA_TRY(cudaGetLastError());
-  ++c->launches;
-  return CLGEN_OK;
-}
+// The counter-stream kernel: one persistent grid, warps claim chunks.  Block
+// shape (CLGEN_BLK_SHAPE or clgen_dev_set_kernel_shape): 0 = 256 threads x 2
+// CTAs/SM, 1 = 256x3, 2 = 256x4 (default), 3 = 128x8; the edge set does not
+// depend on it.
+constexpr int kBlkE = 4;  // gaps per lane per round (part of the stream definition)
 
-// Heavy units (warp-cooperative kernel) then light units (lane-per-unit
-// kernel, occupancy variant CLGEN_CTR_MINB = 2|3|4, default 4: 64 registers).
 template <int MODE>
-int launch_ctr(clgen_dev_ctx* c, const clg::CtrWalkArgs& a_in) {
-  static const int minb = [] {
-    const char* e = std::getenv("CLGEN_CTR_MINB");
-    const int v = e ? std::atoi(e) : 4;
-    return v >= 2 && v <= 4 ? v : 4;
+int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
+  static const int env_shape = [] {
+    const char* e = std::getenv("CLGEN_BLK_SHAPE");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 0 && v <= 3 ? v : 2;
   }();
-  clg::CtrWalkArgs a = a_in;
-  const unsigned long long qstart[2] = {0ull, static_cast<unsigned long long>(c->ctr_heavy)};
-  CUDA_TRY(cudaMemcpyAsync(&c->sc->queue, &qstart[1], sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(&c->sc->queue_heavy, &qstart[0], sizeof(unsigned long long), cudaMemcpyHostToDevice,
-                           c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  if (c->ctr_heavy > 0) {
-    // block shape of the warp kernel: CLGEN_WARP_CFG = 256x4 (default: 64 registers, 32 warps/SM) |
-    // 256x2 | 256x3 | 128x6 | 128x7 | 128x8
-    static const int wcfg_env = [] {
-      const char* e = std::getenv("CLGEN_WARP_CFG");
-      const std::string v = e ? e : "";
-      if (v == "256x2") return 0;
-      if (v == "256x3") return 1;
-      if (v == "128x6") return 3;
-      if (v == "128x7") return 4;
-      if (v == "128x8") return 5;
-      return 2;
-    }();
-    const int wcfg = c->warp_cfg >= 0 ? c->warp_cfg : wcfg_env;
-    const int threads = wcfg >= 3 ? 128 : 256;
-    const size_t smem = clg::ctr_warp_smem_bytes(c->seg_K, c->seg_nb, threads);
-    auto launch = [&](auto kern) -> int {
-      if (!c->ctr_warp_blocks[MODE] || c->ctr_warp_smem[MODE] != smem || c->ctr_warp_cfg[MODE] != wcfg) {
-        if (smem > 48 * 1024)
-          CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        int per_sm = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-        c->ctr_warp_blocks[MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
-        c->ctr_warp_smem[MODE] = smem;
-        c->ctr_warp_cfg[MODE] = wcfg;
-      }
-      const int g = c->ctr_warp_blocks[MODE];
-      a.prof = prof_slots(c, g * threads / 256, true);
-      kern<<<g, threads, smem, c->stream>>>(a, c->split_pos.as<int64_t>(), c->logtab, c->seed_mix, c->ctr_heavy,
-                                             &c->sc->queue_heavy);
-      CUDA_TRY(cudaGetLastError());
-      ++c->launches;
-      return CLGEN_OK;
-    };
-    int rc;
-    switch (wcfg) {
-      case 0: rc = launch(clg::ctr_warp_kernel<MODE, 256, 2>); break;
-      case 1: rc = launch(clg::ctr_warp_kernel<MODE, 256, 3>); break;
-      case 3: rc = launch(clg::ctr_warp_kernel<MODE, 128, 6>); break;
-      case 4: rc = launch(clg::ctr_warp_kernel<MODE, 128, 7>); break;
-      case 5: rc = launch(clg::ctr_warp_kernel<MODE, 128, 8>); break;
-      default: rc = launch(clg::ctr_warp_kernel<MODE, 256, 4>); break;
+  const int shape = c->blk_shape >= 0 ? c->blk_shape : env_shape;
+  clg::BlkArgs a = a_in;
+  CUDA_TRY(cudaMemsetAsync(&c->sc->queue, 0, sizeof(unsigned long long), c->stream));
+  auto launch = [&](auto kern, int threads) -> int {
+    const size_t smem = clg::blk_smem_bytes(threads);
+    if (!c->blk_grid[MODE][shape] || c->blk_smem[MODE][shape] != smem) {
+      if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      int per_sm = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+      c->blk_grid[MODE][shape] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+      c->blk_smem[MODE][shape] = smem;
     }
-    if (rc) return rc;
+    const int g = c->blk_grid[MODE][shape];
+    a.prof = prof_slots(c, g * threads / 256, true);
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    kern<<<g, threads, smem, c->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+    c->timed = true;
+    ++c->launches;
+    return CLGEN_OK;
+  };
+  switch (shape) {
+    case 0: return launch(clg::blk_kernel<MODE, kBlkE, 256, 2>, 256);
+    case 1: return launch(clg::blk_kernel<MODE, kBlkE, 256, 3>, 256);
+    case 3: return launch(clg::blk_kernel<MODE, kBlkE, 128, 8>, 128);
+    default: return launch(clg::blk_kernel<MODE, kBlkE, 256, 4>, 256);
   }
-  if (c->ctr_units > c->ctr_heavy) {
-    int rc;
-    if (minb == 2) rc = launch_ctr_lane<MODE, 2>(c, a, 0);
-    else if (minb == 4) rc = launch_ctr_lane<MODE, 4>(c, a, 2);
-    else rc = launch_ctr_lane<MODE, 3>(c, a, 1);
-    if (rc) return rc;
-  }
-  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
-  c->timed = true;
-  return CLGEN_OK;
 }
 
-// Materialised counter-stream generation (count pass, scan over units, write).
+__global__ void pairs_to_keys_kernel(const uint2* __restrict__ p, int64_t m, unsigned long long* keys) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint2 e = p[i];
+    keys[i] = (static_cast<unsigned long long>(e.x) << 32) | e.y;
+  }
+}
+
+__global__ void keys_to_pairs_kernel(const unsigned long long* __restrict__ keys, int64_t m, uint2* p) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const unsigned long long k = keys[i];
+    p[i] = make_uint2(static_cast<uint32_t>(k >> 32), static_cast<uint32_t>(k));
+  }
+}
+
+// Materialised counter-stream generation: count pass per chunk, scan, write
+// pass at the scanned offsets, then a device radix sort by (u, v) (CUB) so
+// the output order is the reference's (u ascending, then v ascending).
 int materialise_ctr(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t seed, uint32_t* pairs,
                     int64_t cap, int64_t* count) {
   if (cap < 0 || (cap > 0 && !pairs)) return fail(CLGEN_EINVAL, "generate_range: bad output buffer");
   int rc = set_device(c);
   if (rc) return rc;
   if ((rc = reset_scalars(c, 0))) return rc;
-  if (hi == lo || !(S > 0.0)) {
+  if (hi == lo || !(S > 0.0) || c->n < 2) {
     if (count) *count = 0;
     return CLGEN_OK;
   }
-  if ((rc = ensure_ctr_plan(c, S, lo, hi))) return rc;
-  const int64_t U = c->ctr_units;
-  CUDA_TRY(c->unit_counts.ensure((U > 0 ? U : 1) * sizeof(int32_t)));
-  CUDA_TRY(c->offsets.ensure((U > 0 ? U : 1) * sizeof(int64_t)));
-  clg::CtrWalkArgs a = ctr_args(c, S, lo, hi, seed);
-  a.counts = c->unit_counts.as<int32_t>();
-  if ((rc = launch_ctr<clg::kWalkCount>(c, a))) return rc;
-  if ((rc = launch_scan(c, a.counts, c->offsets.as<int64_t>(), U))) return rc;
-  const bool dev_out = is_device_ptr(pairs);
-  uint2* d_pairs = reinterpret_cast<uint2*>(pairs);
-  if (!dev_out) {
-    if ((rc = fetch_scalars(c))) return rc;
-    const int64_t total = c->sc_host->total;
-    const int64_t stage = total < cap ? total : cap;
-    CUDA_TRY(c->pairs.ensure((stage > 0 ? stage : 1) * sizeof(uint2)));
-    d_pairs = c->pairs.as<uint2>();
-    cap = stage;
-  }
-  a.counts = nullptr;
-  a.offsets = c->offsets.as<int64_t>();
-  a.pairs = d_pairs;
-  a.cap = cap;
-  if ((rc = launch_ctr<clg::kWalkWrite>(c, a))) return rc;
-  if (!dev_out && cap > 0)
-    CUDA_TRY(cudaMemcpyAsync(pairs, d_pairs, cap * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = ensure_blocks(c, S))) return rc;
+  if ((rc = ensure_range(c, lo, hi))) return rc;
+  const int64_t U = c->plan_host.chunks_full > 0 ? static_cast<int64_t>(c->plan_host.chunks_full) : 1;
+  CUDA_TRY(c->chunk_counts.ensure(U * sizeof(int32_t)));
+  CUDA_TRY(c->chunk_offsets.ensure(U * sizeof(int64_t)));
+  int64_t units = 0;
+  CUDA_TRY(cudaMemcpyAsync(&units, c->chunk_total.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  clg::BlkArgs a = blk_args(c, S, seed);
+  a.counts = c->chunk_counts.as<int32_t>();
+  if ((rc = launch_blk<clg::kWalkCount>(c, a))) return rc;
+  if ((rc = launch_scan(c, a.counts, c->chunk_offsets.as<int64_t>(), units))) return rc;
   if ((rc = fetch_scalars(c))) return rc;
   const int64_t total = c->sc_host->total;
   if (count) *count = total;
   if (total > cap)
     return fail(CLGEN_ERANGE, "generate_range: %lld edges exceed capacity %lld", (long long)total, (long long)cap);
+  if (total == 0) return CLGEN_OK;
+  CUDA_TRY(c->pairs.ensure(total * sizeof(uint2)));
+  CUDA_TRY(c->keys_a.ensure(total * sizeof(unsigned long long)));
+  CUDA_TRY(c->keys_b.ensure(total * sizeof(unsigned long long)));
+  a.counts = nullptr;
+  a.offsets = c->chunk_offsets.as<int64_t>();
+  a.pairs = c->pairs.as<uint2>();
+  a.cap = total;
+  if ((rc = launch_blk<clg::kWalkWrite>(c, a))) return rc;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, c->num_sms * 16));
+  pairs_to_keys_kernel<<<grid, 256, 0, c->stream>>>(c->pairs.as<uint2>(), total, c->keys_a.as<unsigned long long>());
+  size_t tmp = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, c->keys_a.as<unsigned long long>(),
+                                          c->keys_b.as<unsigned long long>(), total, 0, 64, c->stream));
+  CUDA_TRY(c->sort_tmp.ensure(tmp > 0 ? tmp : 1));
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(c->sort_tmp.p, tmp, c->keys_a.as<unsigned long long>(),
+                                          c->keys_b.as<unsigned long long>(), total, 0, 64, c->stream));
+  uint2* d_out = is_device_ptr(pairs) ? reinterpret_cast<uint2*>(pairs) : c->pairs.as<uint2>();
+  keys_to_pairs_kernel<<<grid, 256, 0, c->stream>>>(c->keys_b.as<unsigned long long>(), total, d_out);
+  c->launches += 3;
+  CUDA_TRY(cudaGetLastError());
+  if (d_out != reinterpret_cast<uint2*>(pairs))
+    CUDA_TRY(cudaMemcpyAsync(pairs, d_out, total * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = fetch_scalars(c))) return rc;
+  if (c->sc_host->overflow)
+    return fail(CLGEN_EINVAL, "generate_range: write pass disagrees with the count pass");
   return CLGEN_OK;
 }
 
@@ -1025,18 +873,10 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->foldtmp.release();
   c->cum.release();
   c->found.release();
-  c->seg_start.release();
-  c->seg_wfirst.release();
-  c->seg_sure.release();
-  c->seg_mass.release();
-  c->seg_em.release();
-  c->seg_invwf.release();
-  c->seg_bucket.release();
-  c->grid_thr.release();
-  c->grid_bounds.release();
-  c->hub_units.release();
-  c->split_pos.release();
-  c->unit_counts.release();
+  for (DevBuf* d : {&c->cls_thr, &c->cls_bounds, &c->cls_start, &c->cls_wfirst, &c->cls_wlast, &c->cls_plan,
+                    &c->blocks, &c->ranges, &c->blk_cnt, &c->blk_prefix, &c->chunk_block, &c->chunk_total,
+                    &c->chunk_counts, &c->chunk_offsets, &c->keys_a, &c->keys_b, &c->sort_tmp})
+    d->release();
   c->probe.release();
   c->prof.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1081,8 +921,8 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
   }
   c->n = 0;
   c->has_runs = false;
-  c->seg_valid = false;
-  c->ctr_lo = c->ctr_hi = -1;
+  c->cls_valid = c->blk_valid = false;
+  c->rng_lo = c->rng_hi = -1;
   c->plan_G = 0;
   if (n > 0) {
     CUDA_TRY(cudaMemcpyAsync(c->w, w, bytes, cudaMemcpyDefault, c->stream));
@@ -1238,14 +1078,15 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   if (degree && (!dev_deg || !accumulate) && ntracked > 0)
     CUDA_TRY(cudaMemsetAsync(d_deg, 0, ntracked * sizeof(uint32_t), c->stream));
   if (stream_mode == CLGEN_STREAM_COUNTER && hi > lo && S > 0.0) {
-    if ((rc = ensure_ctr_plan(c, S, lo, hi))) return rc;
+    if ((rc = ensure_blocks(c, S))) return rc;
+    if ((rc = ensure_range(c, lo, hi))) return rc;
     if ((rc = reset_scalars(c, 0))) return rc;
-    clg::CtrWalkArgs a = ctr_args(c, S, lo, hi, seed);
+    clg::BlkArgs a = blk_args(c, S, seed);
     a.degree = d_deg;
     a.track_shift = track_shift;
     a.ring = reinterpret_cast<uint2*>(ring);
     a.ring_mask = ring ? static_cast<unsigned long long>(ring_cap - 1) : 0ull;
-    if ((rc = launch_ctr<clg::kWalkFold>(c, a))) return rc;
+    if ((rc = launch_blk<clg::kWalkFold>(c, a))) return rc;
   } else {
     if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
     if (hi > lo && stream_mode == CLGEN_STREAM_REFERENCE) {
@@ -1373,24 +1214,23 @@ int clgen_dev_generate_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi,
   return materialise_ctr(c, S, lo, hi, seed, pairs, cap, count);
 }
 
-int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double split_cap) {
+int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chunk_cand) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (!(class_eps > 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be in (0,1]");
-  if (!(split_cap == 0.0 || split_cap >= 32.0)) return fail(CLGEN_EINVAL, "split_cap must be 0 (auto) or >= 32");
-  c->seg_eps = class_eps;
-  c->split_cap = split_cap;
-  c->seg_valid = false;
-  c->ctr_lo = c->ctr_hi = -1;
+  if (!(chunk_cand == 0.0 || (chunk_cand >= 256.0 && chunk_cand <= 1048576.0)))
+    return fail(CLGEN_EINVAL, "chunk_cand must be 0 (default) or in [256, 2^20]");
+  c->cls_eps = class_eps;
+  c->chunk_cand = chunk_cand > 0.0 ? chunk_cand : 32768.0;
+  c->cls_valid = c->blk_valid = false;
+  c->rng_lo = c->rng_hi = -1;
   return CLGEN_OK;
 }
 
-int64_t clgen_dev_counter_heavy_units(clgen_dev_ctx* c) { return c ? c->ctr_heavy : -1; }
-
-int clgen_dev_set_kernel_shape(clgen_dev_ctx* c, int warp_cfg, int deep_lookup) {
+int clgen_dev_set_kernel_shape(clgen_dev_ctx* c, int shape, int flags) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
-  if (warp_cfg < -1 || warp_cfg > 5) return fail(CLGEN_EINVAL, "set_kernel_shape: warp_cfg must be in [-1, 5]");
-  c->warp_cfg = warp_cfg;
-  c->force_deep = deep_lookup != 0;
+  if (shape < -1 || shape > 3) return fail(CLGEN_EINVAL, "set_kernel_shape: shape must be in [-1, 3]");
+  if (flags != 0) return fail(CLGEN_EINVAL, "set_kernel_shape: flags must be 0");
+  c->blk_shape = shape;
   return CLGEN_OK;
 }
 
@@ -1444,11 +1284,15 @@ int clgen_dev_set_fast_math(clgen_dev_ctx* c, int enable) {
   return CLGEN_OK;
 }
 
-int clgen_dev_counter_plan_info(clgen_dev_ctx* c, int* classes, int64_t* hubs, int64_t* units) {
+int clgen_dev_counter_plan_info(clgen_dev_ctx* c, int* classes, int64_t* blocks, int64_t* chunks,
+                                int* dense_blocks, double* class_eps) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
-  if (classes) *classes = c->seg_valid ? c->seg_K : 0;
-  if (hubs) *hubs = c->ctr_H;
-  if (units) *units = c->ctr_units;
+  const bool ok = c->blk_valid;
+  if (classes) *classes = ok ? c->plan_host.K : 0;
+  if (blocks) *blocks = ok ? c->plan_host.nblocks : 0;
+  if (chunks) *chunks = ok ? static_cast<int64_t>(c->plan_host.chunks_full) : 0;
+  if (dense_blocks) *dense_blocks = ok ? c->plan_host.dense_blocks : 0;
+  if (class_eps) *class_eps = ok ? c->plan_host.eps : 0.0;
   return CLGEN_OK;
 }
 

@@ -40,7 +40,7 @@ def test_deterministic_sorted_unique(api, port):
 
 
 def test_streamed_equals_materialised_and_partition_invariant(api, port):
-    w = port.synth_powerlaw(300_000, 2.1, 2.0, 1e5, 9)  # inadmissible head, split hubs
+    w = port.synth_powerlaw(300_000, 2.1, 2.0, 1e5, 9)  # inadmissible head (dense blocks)
     ws = api.make_weight_sequence(w)
     e = api.generate_range(ws, ws.sum_S, 0, w.size, 5)
     full = api.stream_range(ws, ws.sum_S, 0, w.size, 5, mode="counter", track_shift=0)
@@ -48,7 +48,7 @@ def test_streamed_equals_materialised_and_partition_invariant(api, port):
     assert full.checksum == stats.checksum(e)
     deg = np.bincount(e[:, 0], minlength=w.size) + np.bincount(e[:, 1], minlength=w.size)
     np.testing.assert_array_equal(full.degree.astype(np.int64), deg)
-    assert ws.device.counter_plan_info()["hubs"] > 0
+    assert ws.device.counter_plan_info()["dense_blocks"] > 0  # inadmissible head: p = 1 pairs
     # any cover of the sources gives the same graph (UCP plans for 2, 4, 8 GPUs)
     for G in (2, 4, 8):
         b = api.plan_ucp(ws, G)
@@ -92,7 +92,7 @@ def test_degree_chi2(api, name, n, eps):
     import inputs as workloads
     w = workloads.make(name, n)
     ws = api.make_weight_sequence(w)
-    ws.device.set_counter_params(class_eps=eps, split_cap=1024.0)
+    ws.device.set_counter_params(class_eps=eps, chunk_cand=1024.0)
     res = api.stream_range(ws, ws.sum_S, 0, n, 2024, mode="counter", track_shift=0)
     nodes = np.arange(n)
     E, V = stats.expected_degrees(w, ws.sum_S, nodes)
@@ -117,16 +117,15 @@ def test_counter_vs_reference_same_law(api, port):
     assert abs(np.mean(tot_c) - np.mean(tot_r)) < 5 * sd * np.sqrt(2 / 20)
 
 
-def test_heavy_light_split_and_law(api, port):
-    """Both kernels (warp-cooperative heavy units, lane-per-unit light units)
-    run and the joint output keeps the law; heavy/light choice per source is
-    a function of the weights only, so partitions agree."""
+def test_c4_shape_law_and_partitions(api, port):
+    """C4-shaped weights: many class-pair blocks and chunks; the output keeps
+    the law and any UCP cover of the sources gives the same graph."""
     import inputs as workloads
     w = workloads.make("c4", 400_000)
     ws = api.make_weight_sequence(w)
     full = api.stream_range(ws, ws.sum_S, 0, w.size, 99, mode="counter", track_shift=0)
     info = ws.device.counter_plan_info()
-    assert 0 < info["heavy_units"] < info["units"]
+    assert info["blocks"] > 1000 and info["chunks"] > info["blocks"] // 2
     E, V = stats.expected_degrees(w, ws.sum_S, np.arange(w.size))
     z, k = stats.chi2_z(full.degree.astype(np.float64), E, V)
     assert abs(z) <= 5.0, (z, k)
@@ -142,21 +141,19 @@ def test_heavy_light_split_and_law(api, port):
 @pytest.mark.parametrize("name,n", [("c3", 2_000_000), ("c4", 4_000_000), ("c5", 1_000_000)])
 def test_kernel_shape_invariance(api, name, n):
     """The counter-stream graph is a function of (weights, seed) only: every
-    block shape of the heavy-unit kernel (2-4 resident 256-thread blocks,
-    128-thread blocks) and the forward-walk class lookup give the same edge
-    count, checksum and tracked degrees, and the materialised pass matches."""
+    block shape of the sampler (2-4 resident 256-thread CTAs, 128-thread
+    CTAs) gives the same edge count, checksum and tracked degrees, and the
+    materialised pass matches."""
     import inputs as workloads
     w = workloads.make(name, n)
     ws = api.make_weight_sequence(w)
     base = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
-    assert ws.device.counter_plan_info()["heavy_units"] > 0
-    for cfg, deep in ((0, False), (1, False), (2, True), (3, False), (4, False), (5, True)):
-        ws.device.set_kernel_shape(cfg, deep)
+    for cfg in (0, 1, 2, 3):
+        ws.device.set_kernel_shape(cfg)
         r = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
-        assert (r.count, r.checksum) == (base.count, base.checksum), (cfg, deep)
+        assert (r.count, r.checksum) == (base.count, base.checksum), cfg
         np.testing.assert_array_equal(r.degree, base.degree)
-    ws.device.set_kernel_shape(-1, True)
-    e = api.generate_range(ws, ws.sum_S, 0, n, 31)
-    assert len(e) == base.count and stats.checksum(e) == base.checksum
-    canon_ok(e, n)
-    ws.device.set_kernel_shape(-1, False)
+        e = api.generate_range(ws, ws.sum_S, 0, n, 31)
+        assert len(e) == base.count and stats.checksum(e) == base.checksum
+        canon_ok(e, n)
+    ws.device.set_kernel_shape(-1)
