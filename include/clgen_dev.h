@@ -145,8 +145,9 @@ int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, 
 
 /*
  * Streaming generation with fused fold (no materialised edge list):
- * *count = edges, *checksum = sum over edges of mix64((u<<32)|v) mod 2^64
- * (rng.hpp:11-16 finaliser), `degree` (host or device, may be NULL) receives
+ * *count = edges, *checksum = sum over edges of edge_hash(u, v) mod 2^64
+ * (z = ((u<<32)|v) * 0x9e3779b97f4a7c15; z ^= z>>32; z *= 0xd6e8feb86659fd93;
+ * z ^ z>>32 — the fold's own definition, mirrored by the oracle), `degree` (host or device, may be NULL) receives
  * undirected degrees of the tracked nodes x with x % 2^track_shift == 0 at
  * degree[x >> track_shift] (uint32, ceil(n / 2^track_shift) entries; counts
  * are ADDED to the existing contents when `degree` is a device pointer and

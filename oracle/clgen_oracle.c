@@ -142,13 +142,22 @@ int orc_skip_length(double p, double r, int64_t* out) {
   return 0;
 }
 
+/* Checksum term of one edge (the device fold's edge_hash, common.cuh; not a
+ * reference function): multiply / fold / multiply / fold of (u << 32) | v. */
+uint64_t orc_edge_hash(uint64_t u, uint64_t v) {
+  uint64_t z = ((u << 32) | v) * 0x9e3779b97f4a7c15ULL;
+  z ^= z >> 32;
+  z *= 0xd6e8feb86659fd93ULL;
+  return z ^ (z >> 32);
+}
+
 /* Edge consumer: materialise as uint32 pairs and/or fold into a checksum and
  * undirected degree counters. */
 typedef struct {
   uint32_t* pairs;     /* may be NULL */
   int64_t cap;
   int64_t count;
-  uint64_t checksum;   /* sum of mix64((u<<32)|v) mod 2^64 */
+  uint64_t checksum;   /* sum of orc_edge_hash(u, v) mod 2^64 */
   int64_t* degree;     /* may be NULL */
 } orc_sink;
 
@@ -157,7 +166,7 @@ static inline void sink_emit(orc_sink* s, int64_t u, int64_t v) {
     s->pairs[2 * s->count] = (uint32_t)u;
     s->pairs[2 * s->count + 1] = (uint32_t)v;
   }
-  s->checksum += orc_mix64(((uint64_t)u << 32) | (uint64_t)v);
+  s->checksum += orc_edge_hash((uint64_t)u, (uint64_t)v);
   if (s->degree) { ++s->degree[u]; ++s->degree[v]; }
   ++s->count;
 }

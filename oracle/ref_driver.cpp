@@ -74,8 +74,16 @@ class PairSink final : public EdgeSink {
   std::int64_t cap_;
 };
 
-// Order-independent fold: sum of mix64((u<<32)|v) mod 2^64, plus optional
-// per-node undirected degree counters.
+// Order-independent fold: sum of edge_hash(u, v) mod 2^64 (the device fold's
+// checksum term, paper_1406_1215_b200/csrc/common.cuh), plus optional per-node
+// undirected degree counters.
+static std::uint64_t edge_hash(std::uint64_t u, std::uint64_t v) {
+  std::uint64_t z = ((u << 32) | v) * 0x9e3779b97f4a7c15ULL;
+  z ^= z >> 32;
+  z *= 0xd6e8feb86659fd93ULL;
+  return z ^ (z >> 32);
+}
+
 class FoldSink final : public EdgeSink {
  public:
   FoldSink(std::int64_t* degree) : degree_(degree) {}
@@ -83,7 +91,7 @@ class FoldSink final : public EdgeSink {
 
  private:
   void on_edge(const Edge& e) override {
-    checksum += mix64((static_cast<std::uint64_t>(e.u) << 32) | static_cast<std::uint64_t>(e.v));
+    checksum += edge_hash(static_cast<std::uint64_t>(e.u), static_cast<std::uint64_t>(e.v));
     if (degree_) {
       ++degree_[e.u];
       ++degree_[e.v];

@@ -566,6 +566,14 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
     ++c->launches;
     return CLGEN_OK;
   };
+  static const int env_e = [] {
+    const char* e = std::getenv("CLGEN_BLK_E");  // experiment: 8 gaps per lane (a different stream)
+    return e && std::atoi(e) == 8 ? 8 : kBlkE;
+  }();
+  if (env_e == 8) {
+    if (shape == 1) return launch(clg::blk_kernel<MODE, 8, 256, 3>, 256);
+    return launch(clg::blk_kernel<MODE, 8, 256, 2>, 256);
+  }
   switch (shape) {
     case 0: return launch(clg::blk_kernel<MODE, kBlkE, 256, 2>, 256);
     case 1: return launch(clg::blk_kernel<MODE, kBlkE, 256, 3>, 256);

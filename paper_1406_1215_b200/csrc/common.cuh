@@ -16,12 +16,36 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Edge hash of the streaming fold's checksum (sum over edges mod 2^64):
+// multiply / fold / multiply / fold of the 64-bit key (u << 32) | v.  Not a
+// reference function (the reference has no checksum); ten integer
+// instructions per edge on the device.  Mirrored by oracle/clgen_oracle.c
+// (orc_edge_hash), oracle/ref_driver.cpp and tests/stats.py.
+__host__ __device__ __forceinline__ uint64_t edge_hash(uint32_t u, uint32_t v) {
+  uint64_t z = ((static_cast<uint64_t>(u) << 32) | v) * 0x9e3779b97f4a7c15ULL;
+  z ^= z >> 32;
+  z *= 0xd6e8feb86659fd93ULL;
+  return z ^ (z >> 32);
+}
+
 // rng.hpp:20-22
 __host__ __device__ __forceinline__ uint64_t node_rng_key(uint64_t seed, int64_t u) {
   return mix64(seed + static_cast<uint64_t>(u) * 0x9e3779b97f4a7c15ULL);
 }
 
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+// 64-bit rotate as two 32-bit funnel shifts (SHF.L.W), k in [1, 63] constant
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) {
+  const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+  uint32_t nlo, nhi;
+  if (k < 32) {
+    nhi = __funnelshift_l(lo, hi, k);
+    nlo = __funnelshift_l(hi, lo, k);
+  } else {
+    nhi = __funnelshift_l(hi, lo, k - 32);
+    nlo = __funnelshift_l(lo, hi, k - 32);
+  }
+  return (static_cast<uint64_t>(nhi) << 32) | nlo;
+}
 
 // Per-source xoshiro256++ stream, bit-identical to the reference RngStream
 // (rng.hpp:26-69).  Four words live in registers of the lane walking u.

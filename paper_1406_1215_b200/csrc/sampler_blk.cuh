@@ -45,13 +45,13 @@
 namespace clg {
 
 constexpr int kClassCap = 1024;                 // classes (incl. the zero class)
-constexpr int64_t kClassMaxNodes = 1ll << 26;   // nodes per class (block positions < 2^52)
+constexpr int64_t kClassMaxNodes = (1ll << 26) - 64;  // nodes per class (block positions < 2^52 - 2^27)
 constexpr uint32_t kBlkDiag = 1u, kBlkDense = 2u;
 
 struct __align__(16) BlockDesc {
   double pbar;      // RN(RN(w[s_A] w[s_B]) / S): envelope (>= every p_uv of the block)
   double inv_mu;    // 1 / -log1p(-pbar) (sparse blocks)
-  double inv_nb;    // RN(1 / nb)
+  double inv_nb;    // RD(1 / nb) (decode_pos)
   int64_t L;        // chunk length in positions
   int64_t nchunks;  // chunks covering [0, na * nb)
   uint32_t a0, na, b0, nb;
@@ -90,22 +90,26 @@ struct BlkArgs {
   WarpProf prof;
 };
 
-// Exp(1) by inversion from the top 53 bits of x: E = -log(U),
-// U = (x>>11 + 1/2) 2^-53 in (0,1); 128-entry table log + degree-5 log1p,
-// absolute error < 2^-50 (statistically exact).
-__device__ __forceinline__ double exp_bits(uint64_t x, const LogTable& T) {
-  const double u = __dmul_rn(static_cast<double>(x >> 11) + 0.5, 0x1.0p-53);
-  const long long bx = __double_as_longlong(u);
-  const int ex = static_cast<int>((bx >> 52) & 0x7ff) - 1023;
-  const int ti = static_cast<int>((bx >> 45) & (kLogTable - 1));
-  const double m = __longlong_as_double((bx & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-  const double t = __fma_rn(m, T.inv_c[ti], -1.0);
+// E = -log(U) ~ Exp(1) by inversion, U = ((x >> 12) + 1/2) 2^-52 in (0,1)
+// from the top 52 bits of x: y = U 2^52 is built from bits (no int->fp
+// conversion), log y = exponent + table log of the reciprocal centre + a
+// degree-5 log1p series on |t| <= 2^-8; relative error ~2^-47 (statistically
+// exact).  T[i] = {RN(1/c_i), -log RN(1/c_i)}, c_i = 1 + (i + 1/2)/128.
+__device__ __forceinline__ double exp52(uint64_t x, const double2* __restrict__ T) {
+  const double y = __longlong_as_double(static_cast<long long>((x >> 12) | 0x4330000000000000ull)) -
+                   (0x1.0p52 - 0.5);  // (x >> 12) + 1/2, exact
+  const int yh = __double2hiint(y);
+  const int be = yh >> 20;  // biased exponent (y >= 1/2)
+  const int ti = (yh >> 13) & (kLogTable - 1);
+  const double m = __hiloint2double((yh & 0x000fffff) | 0x3ff00000, __double2loint(y));
+  const double2 tc = T[ti];
+  const double t = __fma_rn(m, tc.x, -1.0);
   double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
   sp = __fma_rn(t, sp, 1.0 / 3.0);
   sp = __fma_rn(t, sp, -0.5);
   sp = __fma_rn(t, sp, 1.0);
-  const double e = static_cast<double>(ex);
-  return -__fma_rn(e, 0x1.62e42fefa39efp-1, T.nlog_inv[ti] + __fma_rn(e, 0x1.abc9e3b39803fp-56, t * sp));
+  const double k = __hiloint2double(0x43380000, 1075 - be) - 0x1.8p52;  // 52 - log2 of y's binade, exact
+  return __fma_rn(k, 0x1.62e42fefa39efp-1, __fma_rn(k, 0x1.abc9e3b39803fp-56, -__fma_rn(t, sp, tc.y)));
 }
 
 __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
@@ -134,28 +138,17 @@ __device__ __forceinline__ double warp_incl_scan_f64(double x) {
   return x;
 }
 
-__device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t x, uint32_t& total) {
-  const int lane = lane_id();
-  uint32_t s = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(CLG_FULL, s, o);
-    if (lane >= o) s += y;
-  }
-  total = __shfl_sync(CLG_FULL, s, 31);
-  return s - x;
-}
-
 // (row, col) of row-major position x (exact integer double < 2^52) in a
-// block of nb columns: quotient from RN(1/nb), corrected by the exact residual.
-__device__ __forceinline__ void decode_pos(double x, double inv_nb, double nb_d, int32_t nb, uint32_t& row,
+// block of nb columns.  The quotient is rounded down twice (inv_nb_rd =
+// RD(1/nb), RD product), so it is the true quotient or one less; the exact
+// residual x - row nb in [0, 2 nb) settles it.  No int <-> fp conversions:
+// the integers are read from the low word of 2^52 + value.
+__device__ __forceinline__ void decode_pos(double x, double inv_nb_rd, double nb_d, int32_t nb, uint32_t& row,
                                            uint32_t& col) {
-  uint32_t r = __double2uint_rz(x * inv_nb);
-  int32_t c = __double2int_rz(__fma_rn(-static_cast<double>(r), nb_d, x));
-  if (c < 0) {
-    c += nb;
-    --r;
-  } else if (c >= nb) {
+  const double qf = __dadd_rd(__dmul_rd(x, inv_nb_rd), 0x1.0p52);  // 2^52 + floor(q)
+  uint32_t r = static_cast<uint32_t>(__double2loint(qf));
+  int32_t c = __double2loint(__fma_rn(-(qf - 0x1.0p52), nb_d, x) + 0x1.0p52);
+  if (c >= nb) {
     c -= nb;
     ++r;
   }
@@ -163,42 +156,44 @@ __device__ __forceinline__ void decode_pos(double x, double inv_nb, double nb_d,
   col = static_cast<uint32_t>(c);
 }
 
-constexpr int kStageCap = 256;  // staged pairs per warp (ring / write modes)
+constexpr int kStageCap = 512;  // staged pairs per warp (ring / write modes)
 constexpr int kUncCap = 64;     // queued uncertain candidates per warp
 
 __host__ __device__ inline size_t blk_smem_bytes(int threads) {
-  return sizeof(LogTable) + static_cast<size_t>(threads / 32) * (kStageCap * sizeof(uint2) + kUncCap * 16);
+  return kLogTable * sizeof(double2) +
+         static_cast<size_t>(threads / 32) * (kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4) + 16);
 }
+
+// Per-warp chunk constants needed only on the rare paths (uncertain
+// candidates), kept in shared memory instead of registers.
+struct WarpChunk {
+  uint64_t key;
+  double pbar;
+};
 
 template <int MODE, int E, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LogTable& s_log = *reinterpret_cast<LogTable*>(smem_raw);
+  double2* s_log = reinterpret_cast<double2*>(smem_raw);
   const int wib = threadIdx.x >> 5;
-  uint2* stage = reinterpret_cast<uint2*>(smem_raw + sizeof(LogTable)) + wib * kStageCap;
-  uint32_t* qbase = reinterpret_cast<uint32_t*>(smem_raw + sizeof(LogTable) +
-                                                (THREADS / 32) * kStageCap * sizeof(uint2)) + wib * 4 * kUncCap;
-  uint32_t* qu = qbase;
-  uint32_t* qv = qbase + kUncCap;
-  uint32_t* qh = qbase + 2 * kUncCap;
-  uint32_t* qi = qbase + 3 * kUncCap;
-  for (int i = threadIdx.x; i < kLogTable; i += THREADS) {
-    s_log.inv_c[i] = a.logtab->inv_c[i];
-    s_log.nlog_inv[i] = a.logtab->nlog_inv[i];
-  }
+  unsigned char* wbase = smem_raw + kLogTable * sizeof(double2) +
+                         static_cast<size_t>(wib) * (kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4) + 16);
+  uint2* stage = reinterpret_cast<uint2*>(wbase);
+  uint2* quv = reinterpret_cast<uint2*>(wbase + kStageCap * sizeof(uint2));
+  uint32_t* qh = reinterpret_cast<uint32_t*>(wbase + kStageCap * sizeof(uint2) + kUncCap * sizeof(uint2));
+  WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wbase + kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4));
+  for (int i = threadIdx.x; i < kLogTable; i += THREADS) s_log[i] = make_double2(a.logtab->inv_c[i], a.logtab->nlog_inv[i]);
   __syncthreads();
 
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
-  const double* __restrict__ w = a.w;
-  const double S = a.S;
   const int64_t total = *a.total_chunks;
   const uint32_t tmask = (1u << a.track_shift) - 1u;
-  const bool track = a.degree != nullptr;
+  const bool track = MODE == kWalkFold && a.degree != nullptr;
 
   // fold-mode ring: a private circular segment per warp (no reservation atomics)
-  uint2* seg = nullptr;
+  uint2* seg = nullptr;  // null: fold only
   uint32_t smask = 0, wpos = 0;
   if (MODE == kWalkFold && a.ring) {
     const unsigned nw = gridDim.x * (THREADS >> 5);
@@ -211,24 +206,39 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     smask = (1u << sl) - 1u;
     seg = a.ring + ((static_cast<unsigned long long>(gw) << sl) & a.ring_mask);
   }
-  const bool staging = (MODE == kWalkFold && seg != nullptr) || MODE == kWalkWrite;
+  constexpr bool staging = MODE != kWalkCount;  // fold: every edge is staged (fold + ring at flush)
   uint32_t head = 0, tail = 0;  // stage counters (warp-uniform)
   uint64_t checksum = 0;
-  uint32_t edges = 0;           // fold: per lane; count: per lane within the chunk
+  uint64_t wedges = 0;          // edges of this warp
   int64_t out_pos = 0;          // write mode
   Xoro128 rng;
 
-  // flush 64 staged pairs as one 512-byte burst (ring: 16-byte vectors)
+  // fold of one staged edge: checksum term and tracked degrees
+  auto fold_pair = [&](uint2 e, bool live) {
+    checksum += live ? edge_hash(e.x, e.y) : 0ull;
+    if (track) {
+      const bool tu = live && (e.x & tmask) == 0, tv = live && (e.y & tmask) == 0;
+      if (__any_sync(CLG_FULL, tu || tv)) {
+        if (tu) atomicAdd(&a.degree[e.x >> a.track_shift], 1u);
+        if (tv) atomicAdd(&a.degree[e.y >> a.track_shift], 1u);
+      }
+    }
+  };
+  // flush 64 staged pairs: fold them (2 per lane, every lane busy) and write
+  // them as one 512-byte burst (ring: 16-byte vector stores)
   auto flush64 = [&]() {
     __syncwarp();
     if (MODE == kWalkFold) {
       const uint4 v2 = *reinterpret_cast<const uint4*>(&stage[(tail + 2 * lane) & (kStageCap - 1)]);
-      *reinterpret_cast<uint4*>(&seg[(wpos + 2 * lane) & smask]) = v2;
+      fold_pair(make_uint2(v2.x, v2.y), true);
+      fold_pair(make_uint2(v2.z, v2.w), true);
+      if (seg) *reinterpret_cast<uint4*>(&seg[(wpos + 2 * lane) & smask]) = v2;
       wpos += 64;
     } else {
-      for (int i = lane; i < 64; i += 32) {
-        const int64_t p = out_pos + i;
-        if (p < a.cap) a.pairs[p] = stage[(tail + i) & (kStageCap - 1)];
+#pragma unroll
+      for (int i = 0; i < 64; i += 32) {
+        const int64_t p = out_pos + i + lane;
+        if (p < a.cap) a.pairs[p] = stage[(tail + i + lane) & (kStageCap - 1)];
         else atomicAdd(a.overflow, 1ull);
       }
       out_pos += 64;
@@ -239,12 +249,14 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   auto flush_rest = [&]() {  // < 64 left
     __syncwarp();
     const uint32_t rem = head - tail;
-    for (uint32_t i = lane; i < rem; i += 32) {
-      const uint2 e = stage[(tail + i) & (kStageCap - 1)];
+    for (uint32_t i0 = 0; i0 < rem; i0 += 32) {
+      const bool live = i0 + lane < rem;
+      const uint2 e = stage[(tail + i0 + lane) & (kStageCap - 1)];
       if (MODE == kWalkFold) {
-        seg[(wpos + i) & smask] = e;
-      } else {
-        const int64_t p = out_pos + i;
+        fold_pair(e, live);
+        if (seg && live) seg[(wpos + i0 + lane) & smask] = e;
+      } else if (live) {
+        const int64_t p = out_pos + i0 + lane;
         if (p < a.cap) a.pairs[p] = e;
         else atomicAdd(a.overflow, 1ull);
       }
@@ -254,13 +266,16 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     tail = head;
     __syncwarp();
   };
-  // emission of up to N pairs per lane (lane-major)
-  auto fold_one = [&](uint32_t u, uint32_t v) {
-    checksum += mix64((static_cast<uint64_t>(u) << 32) | v);
-    if (track) {
-      if ((u & tmask) == 0) atomicAdd(&a.degree[u >> a.track_shift], 1u);
-      if ((v & tmask) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
+  uint32_t cw = 0;  // edges of the current chunk (warp-uniform)
+  // one candidate slot per lane: stage the accepted pairs
+  auto emit1 = [&](bool acc, uint32_t u, uint32_t v) {
+    const unsigned b = __ballot_sync(CLG_FULL, acc);
+    const uint32_t nb = __popc(b);
+    if (staging) {
+      if (acc) stage[(head + __popc(b & lt)) & (kStageCap - 1)] = make_uint2(u, v);
+      head += nb;
     }
+    cw += nb;
   };
 
   for (;;) {
@@ -276,37 +291,24 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     const int64_t x0 = c * d.L;
     const int64_t x1 = imin64(x0 + d.L, N);
     const double xend = static_cast<double>(x1);
-    const double wlo = static_cast<double>(imax64(x0, r.x_lo));
-    const double whi = static_cast<double>(imin64(x1, r.x_hi));
+    // a chunk cut by the launch's source range emits only the rows inside it
+    const bool partial = r.x_lo > x0 || r.x_hi < x1;
     const uint64_t key = mix64(a.seed_mix ^ (static_cast<uint64_t>(b) | (static_cast<uint64_t>(c) << 20)));
     rng.seed_key(key + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1));
+    __syncwarp();
+    if (lane == 0) {
+      wc.key = key;
+      wc.pbar = d.pbar;
+    }
+    __syncwarp();
     const bool diag = (d.flags & kBlkDiag) != 0;
     const double nb_d = static_cast<double>(d.nb);
     const int32_t nbi = static_cast<int32_t>(d.nb);
     uint32_t qn = 0, qt = 0;  // uncertain queue counters (warp-uniform)
     if (MODE == kWalkWrite) out_pos = a.offsets[q];
-    if (MODE == kWalkCount) edges = 0;
+    cw = 0;
+    const double wlo = static_cast<double>(r.x_lo), whi = static_cast<double>(r.x_hi);
 
-    auto emit = [&](const bool* acc, const uint32_t* uu, const uint32_t* vv, int n) {
-      uint32_t cnt = 0;
-      for (int e = 0; e < n; ++e) cnt += acc[e] ? 1u : 0u;
-      if (MODE == kWalkCount) {
-        edges += cnt;
-        return;
-      }
-      if (MODE == kWalkFold) {
-        edges += cnt;
-        for (int e = 0; e < n; ++e)
-          if (acc[e]) fold_one(uu[e], vv[e]);
-      }
-      if (!staging) return;
-      uint32_t tot;
-      uint32_t pos = head + warp_excl_scan_u32(cnt, tot);
-      for (int e = 0; e < n; ++e)
-        if (acc[e]) stage[(pos++) & (kStageCap - 1)] = make_uint2(uu[e], vv[e]);
-      head += tot;
-      while (head - tail >= 64) flush64();
-    };
     // decide the queued uncertain candidates (k <= 32): gather w_u, w_v
     auto resolve = [&](uint32_t k) {
       __syncwarp();
@@ -314,16 +316,18 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       uint32_t u = 0, v = 0;
       if (static_cast<uint32_t>(lane) < k) {
         const uint32_t i = (qt + lane) & (kUncCap - 1);
-        u = qu[i];
-        v = qv[i];
-        const double wu = w[u], wv = w[v];
-        const double qv_ = __ddiv_rn(__dmul_rn(wu, wv), S);  // edge_skip.cpp:36
-        const double p = qv_ < 1.0 ? qv_ : 1.0;
-        acc = lazy_accept(qh[i], __ddiv_rn(p, d.pbar), key, qi[i]);
+        const uint2 uv = quv[i];
+        const uint32_t hid = qh[i];
+        u = uv.x;
+        v = uv.y;
+        const double q_ = __ddiv_rn(__dmul_rn(a.w[u], a.w[v]), a.S);  // edge_skip.cpp:36
+        acc = lazy_accept(hid & 2047u, __ddiv_rn(q_ < 1.0 ? q_ : 1.0, wc.pbar), wc.key, hid >> 11);
       }
       qt += k;
       __syncwarp();
-      emit(&acc, &u, &v, 1);
+      emit1(acc, u, v);
+      if (staging)
+        while (head - tail >= 64) flush64();
     };
 
     if (!(d.flags & kBlkDense)) {
@@ -331,85 +335,81 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       const double inv_mu = d.inv_mu, inv_nb = d.inv_nb;
       const uint32_t hs = d.hs;
       double base = static_cast<double>(x0);  // next candidate is at >= base
-      for (uint32_t rid = 0;; ++rid) {
+      for (uint32_t idb = static_cast<uint32_t>(lane) * E;; idb += 32u * E) {  // candidate id base
         double pos[E];
         uint32_t hh[E];
         double s = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const uint64_t x = rng.next();
-          const double g = fmin(floor(exp_bits(x, s_log) * inv_mu), 0x1.0p52);
-          s += g + 1.0;
+          // geometric gap floor(E / mu) + 1 (>= 2^52: past every chunk end)
+          s += __dadd_rd(exp52(x, s_log) * inv_mu, 0x1.0p52) - (0x1.0p52 - 1.0);
           pos[e] = s;
           hh[e] = static_cast<uint32_t>(x) & 2047u;
         }
         const double incl = warp_incl_scan_f64(s);
         const double lb = base + (incl - s) - 1.0;
-        const double last = __shfl_sync(CLG_FULL, lb + s, 31);
-        bool sure[E];
-        uint32_t uu[E], vv[E];
+        const double last = base + __shfl_sync(CLG_FULL, incl, 31) - 1.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const double x = lb + pos[e];
           uint32_t row, col;
           decode_pos(x, inv_nb, nb_d, nbi, row, col);
-          const bool ok = x < whi && x >= wlo && (!diag || col > row);
-          uu[e] = d.a0 + row;
-          vv[e] = d.b0 + col;
-          sure[e] = ok && hh[e] < hs;
-          const bool unc = ok && !sure[e];
+          bool ok = x < xend && (col > row || !diag);
+          if (partial) ok = ok && x >= wlo && x < whi;
+          const uint32_t u = d.a0 + row, v = d.b0 + col;
+          const bool sure = ok && hh[e] < hs;
+          emit1(sure, u, v);
+          const bool unc = ok && !sure;
           const unsigned m = __ballot_sync(CLG_FULL, unc);
           if (m) {
             if (unc) {
               const uint32_t i = (qn + __popc(m & lt)) & (kUncCap - 1);
-              qu[i] = uu[e];
-              qv[i] = vv[e];
-              qh[i] = hh[e];
-              qi[i] = rid * (32u * E) + static_cast<uint32_t>(lane) * E + e;
+              quv[i] = make_uint2(u, v);
+              qh[i] = hh[e] | (((idb + e) & 0x1fffffu) << 11);
             }
             qn += __popc(m);
             if (qn - qt >= 32) resolve(32);
           }
         }
-        emit(sure, uu, vv, E);
+        if (staging)
+          while (head - tail >= 64) flush64();
         if (!(last < xend)) break;
         base = last + 1.0;
       }
     } else {
       // ---- dense block (pbar >= 1): every position is a candidate ----
       const double inv_nb = d.inv_nb;
-      const double x0d = static_cast<double>(x0);
-      for (double xb = x0d; xb < xend; xb += 32.0) {
+      for (double xb = static_cast<double>(x0); xb < xend; xb += 32.0) {
         const double x = xb + static_cast<double>(lane);
         uint32_t row, col;
         decode_pos(x, inv_nb, nb_d, nbi, row, col);
-        const bool cand = x < xend && (!diag || col > row);
+        const bool cand = x < xend && (col > row || !diag);
         const uint32_t u = d.a0 + row, v = d.b0 + col;
         bool acc = false;
         if (cand) {
-          const double q_ = __ddiv_rn(__dmul_rn(w[u], w[v]), S);
+          const double q_ = __ddiv_rn(__dmul_rn(a.w[u], a.w[v]), a.S);
           // the draw is taken for every candidate below 1, emitted or not, so
           // the stream does not depend on the launch's window
           acc = q_ >= 1.0 || unit53(rng.next()) < q_;
-          acc = acc && x >= wlo && x < whi;
+          if (partial) acc = acc && x >= wlo && x < whi;
         }
-        emit(&acc, &u, &v, 1);
+        emit1(acc, u, v);
+        if (staging)
+          while (head - tail >= 64) flush64();
       }
     }
     if (qn != qt) resolve(qn - qt);
-    if (MODE == kWalkCount) {
-      const uint32_t ce = static_cast<uint32_t>(warp_sum(static_cast<int64_t>(edges)));
-      if (lane == 0) a.counts[q] = static_cast<int32_t>(ce);
-    }
+    if (MODE == kWalkCount && lane == 0) a.counts[q] = static_cast<int32_t>(cw);
+    wedges += cw;
     if (MODE == kWalkWrite) flush_rest();
   }
 
   if (MODE == kWalkFold) {
-    if (staging) flush_rest();
+    flush_rest();
     const uint64_t cs = warp_sum_u64(checksum);
-    const uint64_t es = warp_sum_u64(static_cast<uint64_t>(edges));
     if (lane == 0) {
-      atomicAdd(&a.fold_out[0], static_cast<unsigned long long>(es));
+      atomicAdd(&a.fold_out[0], static_cast<unsigned long long>(wedges));
       atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(cs));
     }
   }
@@ -546,12 +546,13 @@ __global__ void blk_desc_kernel(const int64_t* __restrict__ start, const double*
   d.flags = A == B ? kBlkDiag : 0u;
   const double pbar = __ddiv_rn(__dmul_rn(wfirst[A], wfirst[B]), S);
   d.pbar = pbar;
-  d.inv_nb = 1.0 / static_cast<double>(d.nb);
+  d.inv_nb = __drcp_rd(static_cast<double>(d.nb));
   const int64_t N = static_cast<int64_t>(d.na) * d.nb;
   d.inv_mu = 0.0;
   d.hs = 0;
   int64_t L;
-  if (!(pbar > 0.0) || N == 0 || (A == B && d.na < 2)) {
+  // pbar < 2^-900: below 2^-848 expected edges in the block, treated as empty
+  if (!(pbar >= 0x1.0p-900) || N == 0 || (A == B && d.na < 2)) {
     L = 1;
     d.nchunks = 0;
   } else if (pbar >= 1.0) {

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         }
         ++out_pos;
       } else if (MODE == kWalkFold) {
-        checksum += mix64((static_cast<uint64_t>(u) << 32) | static_cast<uint64_t>(v));
+        checksum += edge_hash(static_cast<uint32_t>(u), static_cast<uint32_t>(v));
         ++edges_total;
         if (a.degree && (v & ((1ll << a.track_shift) - 1)) == 0) atomicAdd(&a.degree[v >> a.track_shift], 1u);
       }

@@ -64,6 +64,15 @@ def mix64_np(z):
         return z ^ (z >> np.uint64(31))
 
 
+def edge_hash_np(u, v):
+    """The fold checksum's per-edge term (common.cuh edge_hash)."""
+    with np.errstate(over="ignore"):
+        z = ((u.astype(np.uint64) << np.uint64(32)) | v.astype(np.uint64)) * np.uint64(0x9E3779B97F4A7C15)
+        z ^= z >> np.uint64(32)
+        z *= np.uint64(0xD6E8FEB86659FD93)
+        return z ^ (z >> np.uint64(32))
+
+
 def checksum(pairs: np.ndarray) -> int:
-    p = pairs.astype(np.uint64)
-    return int(mix64_np((p[:, 0] << np.uint64(32)) | p[:, 1]).sum(dtype=np.uint64))
+    """Sum over edges of edge_hash(u, v) mod 2^64 (the streaming fold's checksum)."""
+    return int(edge_hash_np(pairs[:, 0], pairs[:, 1]).sum(dtype=np.uint64))

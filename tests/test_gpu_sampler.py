@@ -6,6 +6,8 @@ import os
 import numpy as np
 import pytest
 
+import stats
+
 from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
@@ -140,16 +142,7 @@ def test_ring_emission_matches_checksum(api, port):
     r = ring.cpu().numpy().view(np.uint32).astype(np.uint64)
     nz = r[(r[:, 0] != 0) | (r[:, 1] != 0)]
     assert len(nz) == cnt
-    assert int(mix64_np((nz[:, 0] << np.uint64(32)) | nz[:, 1]).sum(dtype=np.uint64)) == cks
-
-
-def mix64_np(z):
-    """Vectorised splitmix64 finaliser (rng.hpp:11-16), wrapping uint64."""
-    with np.errstate(over="ignore"):
-        z = z + np.uint64(0x9E3779B97F4A7C15)
-        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        return z ^ (z >> np.uint64(31))
+    assert stats.checksum(nz) == cks
 
 
 def test_fast_math_identical_to_reference_expressions(api, port):
