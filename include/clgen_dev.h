@@ -126,8 +126,8 @@ int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
 
 /* Counter-stream kernel shape (no reference counterpart; the edge set does
- * not depend on it): 0 = 256 threads x 2 CTAs/SM, 1 = 256x3, 2 = 256x4
- * (default), 3 = 128x8, -1 = CLGEN_BLK_SHAPE or the default.  flags must be
+ * not depend on it): 256 threads x 2 / 3 / 4 (default) / 5 / 6 CTAs per SM
+ * for shape 0 / 1 / 2 / 3 / 4, -1 = CLGEN_BLK_SHAPE or the default.  flags must be
  * 0.  Used by the schedule-invariance tests. */
 int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int shape, int flags);
 int clgen_dev_warp_profile_launches(clgen_dev_ctx* ctx);

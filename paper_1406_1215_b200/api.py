@@ -148,8 +148,8 @@ class Device:
         check(_lib.lib().clgen_dev_set_fast_math(self._h, int(bool(enable))))
 
     def set_kernel_shape(self, shape: int = -1) -> None:
-        """Counter-stream kernel block shape (0: 256x2, 1: 256x3, 2: 256x4,
-        3: 128x8 threads x CTAs/SM; -1 default); the edge set does not depend on it."""
+        """Counter-stream kernel shape: 256 threads x 2/3/4/5/6 CTAs per SM for
+        shape 0/1/2/3/4 (-1: default 2); the edge set does not depend on it."""
         check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(shape), 0))
 
     def set_warp_profile(self, enable: bool = True) -> None:

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <vector>
+#include <type_traits>
 #include <string>
 
 #include "../../include/clgen_dev.h"
@@ -145,8 +146,8 @@ struct clgen_dev_ctx {
   double cls_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
   double chunk_cand = env_double("CLGEN_CTR_CHUNK", 32768.0);
   int blk_shape = -1;  // clgen_dev_set_kernel_shape (-1: CLGEN_BLK_SHAPE / default)
-  int blk_grid[3][4] = {};
-  size_t blk_smem[3][4] = {};
+  int blk_grid[3][5] = {};
+  size_t blk_smem[3][5] = {};
   // optional per-warp busy intervals of the sampler kernels
   bool warp_prof = false;
   DevBuf prof;
@@ -531,17 +532,17 @@ clg::BlkArgs blk_args(clgen_dev_ctx* c, double S, uint64_t seed) {
 }
 
 // The counter-stream kernel: one persistent grid, warps claim chunks.  Block
-// shape (CLGEN_BLK_SHAPE or clgen_dev_set_kernel_shape): 0 = 256 threads x 2
-// CTAs/SM, 1 = 256x3, 2 = 256x4 (default), 3 = 128x8; the edge set does not
-// depend on it.
-constexpr int kBlkE = 4;  // gaps per lane per round (part of the stream definition)
+// shape (CLGEN_BLK_SHAPE or clgen_dev_set_kernel_shape): 256 threads x
+// 2 / 3 / 4 (default) / 5 / 6 CTAs per SM for shape 0 / 1 / 2 / 3 / 4; the
+// edge set does not depend on it.
+constexpr int kBlkE = 4;  // candidates per lane per loop iteration (an unroll factor)
 
 template <int MODE>
 int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
   static const int env_shape = [] {
     const char* e = std::getenv("CLGEN_BLK_SHAPE");
     const int v = e ? std::atoi(e) : 2;
-    return v >= 0 && v <= 3 ? v : 2;
+    return v >= 0 && v <= 4 ? v : 2;
   }();
   const int shape = c->blk_shape >= 0 ? c->blk_shape : env_shape;
   clg::BlkArgs a = a_in;
@@ -567,19 +568,23 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
     return CLGEN_OK;
   };
   static const int env_e = [] {
-    const char* e = std::getenv("CLGEN_BLK_E");  // experiment: 8 gaps per lane (a different stream)
-    return e && std::atoi(e) == 8 ? 8 : kBlkE;
+    const char* e = std::getenv("CLGEN_BLK_E");  // candidates per lane per loop iteration (unroll; same stream)
+    const int v = e ? std::atoi(e) : kBlkE;
+    return v == 2 ? 2 : (v == 1 ? 1 : kBlkE);
   }();
-  if (env_e == 8) {
-    if (shape == 1) return launch(clg::blk_kernel<MODE, 8, 256, 3>, 256);
-    return launch(clg::blk_kernel<MODE, 8, 256, 2>, 256);
-  }
-  switch (shape) {
-    case 0: return launch(clg::blk_kernel<MODE, kBlkE, 256, 2>, 256);
-    case 1: return launch(clg::blk_kernel<MODE, kBlkE, 256, 3>, 256);
-    case 3: return launch(clg::blk_kernel<MODE, kBlkE, 128, 8>, 128);
-    default: return launch(clg::blk_kernel<MODE, kBlkE, 256, 4>, 256);
-  }
+  auto by_shape = [&](auto e_tag) -> int {
+    constexpr int EE = decltype(e_tag)::value;
+    switch (shape) {
+      case 0: return launch(clg::blk_kernel<MODE, EE, 256, 2>, 256);
+      case 1: return launch(clg::blk_kernel<MODE, EE, 256, 3>, 256);
+      case 3: return launch(clg::blk_kernel<MODE, EE, 256, 5>, 256);
+      case 4: return launch(clg::blk_kernel<MODE, EE, 256, 6>, 256);
+      default: return launch(clg::blk_kernel<MODE, EE, 256, 4>, 256);
+    }
+  };
+  if (env_e == 1) return by_shape(std::integral_constant<int, 1>{});
+  if (env_e == 2) return by_shape(std::integral_constant<int, 2>{});
+  return by_shape(std::integral_constant<int, kBlkE>{});
 }
 
 __global__ void pairs_to_keys_kernel(const uint2* __restrict__ p, int64_t m, unsigned long long* keys) {
@@ -1236,7 +1241,7 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chun
 
 int clgen_dev_set_kernel_shape(clgen_dev_ctx* c, int shape, int flags) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
-  if (shape < -1 || shape > 3) return fail(CLGEN_EINVAL, "set_kernel_shape: shape must be in [-1, 3]");
+  if (shape < -1 || shape > 4) return fail(CLGEN_EINVAL, "set_kernel_shape: shape must be in [-1, 4]");
   if (flags != 0) return fail(CLGEN_EINVAL, "set_kernel_shape: flags must be 0");
   c->blk_shape = shape;
   return CLGEN_OK;

@@ -95,14 +95,14 @@ struct BlkArgs {
 // conversion), log y = exponent + table log of the reciprocal centre + a
 // degree-5 log1p series on |t| <= 2^-8; relative error ~2^-47 (statistically
 // exact).  T[i] = {RN(1/c_i), -log RN(1/c_i)}, c_i = 1 + (i + 1/2)/128.
-__device__ __forceinline__ double exp52(uint64_t x, const double2* __restrict__ T) {
-  const double y = __longlong_as_double(static_cast<long long>((x >> 12) | 0x4330000000000000ull)) -
-                   (0x1.0p52 - 0.5);  // (x >> 12) + 1/2, exact
+__device__ __forceinline__ double exp52_y(uint64_t x) {  // (x >> 12) + 1/2, exact
+  return __longlong_as_double(static_cast<long long>((x >> 12) | 0x4330000000000000ull)) - (0x1.0p52 - 0.5);
+}
+__device__ __forceinline__ int exp52_index(double y) { return (__double2hiint(y) >> 13) & (kLogTable - 1); }
+__device__ __forceinline__ double exp52_tab(double y, double2 tc) {
   const int yh = __double2hiint(y);
   const int be = yh >> 20;  // biased exponent (y >= 1/2)
-  const int ti = (yh >> 13) & (kLogTable - 1);
   const double m = __hiloint2double((yh & 0x000fffff) | 0x3ff00000, __double2loint(y));
-  const double2 tc = T[ti];
   const double t = __fma_rn(m, tc.x, -1.0);
   double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
   sp = __fma_rn(t, sp, 1.0 / 3.0);
@@ -110,6 +110,10 @@ __device__ __forceinline__ double exp52(uint64_t x, const double2* __restrict__ 
   sp = __fma_rn(t, sp, 1.0);
   const double k = __hiloint2double(0x43380000, 1075 - be) - 0x1.8p52;  // 52 - log2 of y's binade, exact
   return __fma_rn(k, 0x1.62e42fefa39efp-1, __fma_rn(k, 0x1.abc9e3b39803fp-56, -__fma_rn(t, sp, tc.y)));
+}
+__device__ __forceinline__ double exp52(uint64_t x, const double2* __restrict__ T) {
+  const double y = exp52_y(x);
+  return exp52_tab(y, T[exp52_index(y)]);
 }
 
 __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
@@ -224,8 +228,11 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       }
     }
   };
-  // flush 64 staged pairs: fold them (2 per lane, every lane busy) and write
-  // them as one 512-byte burst (ring: 16-byte vector stores)
+  // flush 64 staged pairs.  Fold mode folds them (2 per lane, every lane
+  // busy) and writes them into the warp's ring segment as one 512-byte burst
+  // of 16-byte vector stores (measured faster here than handing the region to
+  // the TMA engine with cp.async.bulk, whose issue/wait serialises on one
+  // lane); write mode stores them at the chunk's output offset.
   auto flush64 = [&]() {
     __syncwarp();
     if (MODE == kWalkFold) {
@@ -331,34 +338,30 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     };
 
     if (!(d.flags & kBlkDense)) {
-      // ---- sparse block: geometric gaps, E per lane per round ----
+      // ---- sparse block: each lane runs its own geometric process over its
+      // 1/32 of the chunk (memoryless restart at the lane's first position:
+      // no cross-lane dependence), E candidates per iteration ----
       const double inv_mu = d.inv_mu, inv_nb = d.inv_nb;
       const uint32_t hs = d.hs;
-      double base = static_cast<double>(x0);  // next candidate is at >= base
-      for (uint32_t idb = static_cast<uint32_t>(lane) * E;; idb += 32u * E) {  // candidate id base
-        double pos[E];
-        uint32_t hh[E];
-        double s = 0.0;
+      const int64_t ls = (x1 - x0 + 31) >> 5;
+      const int64_t lx0 = imin64(x0 + lane * ls, x1);
+      const double lend = static_cast<double>(imin64(lx0 + ls, x1));
+      double pos = static_cast<double>(lx0) - 1.0;  // last candidate position
+      bool live = pos + 1.0 < lend;
+      for (uint32_t id = 0; __any_sync(CLG_FULL, live); id += E) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const uint64_t x = rng.next();
           // geometric gap floor(E / mu) + 1 (>= 2^52: past every chunk end)
-          s += __dadd_rd(exp52(x, s_log) * inv_mu, 0x1.0p52) - (0x1.0p52 - 1.0);
-          pos[e] = s;
-          hh[e] = static_cast<uint32_t>(x) & 2047u;
-        }
-        const double incl = warp_incl_scan_f64(s);
-        const double lb = base + (incl - s) - 1.0;
-        const double last = base + __shfl_sync(CLG_FULL, incl, 31) - 1.0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const double x = lb + pos[e];
+          pos += __dadd_rd(exp52(x, s_log) * inv_mu, 0x1.0p52) - (0x1.0p52 - 1.0);
+          live = live && pos < lend;
           uint32_t row, col;
-          decode_pos(x, inv_nb, nb_d, nbi, row, col);
-          bool ok = x < xend && (col > row || !diag);
-          if (partial) ok = ok && x >= wlo && x < whi;
+          decode_pos(pos, inv_nb, nb_d, nbi, row, col);
+          bool ok = live && (col > row || !diag);
+          if (partial) ok = ok && pos >= wlo && pos < whi;
           const uint32_t u = d.a0 + row, v = d.b0 + col;
-          const bool sure = ok && hh[e] < hs;
+          const uint32_t h = static_cast<uint32_t>(x) & 2047u;
+          const bool sure = ok && h < hs;
           emit1(sure, u, v);
           const bool unc = ok && !sure;
           const unsigned m = __ballot_sync(CLG_FULL, unc);
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
             if (unc) {
               const uint32_t i = (qn + __popc(m & lt)) & (kUncCap - 1);
               quv[i] = make_uint2(u, v);
-              qh[i] = hh[e] | (((idb + e) & 0x1fffffu) << 11);
+              qh[i] = h | ((((id + e) << 5 | static_cast<uint32_t>(lane)) & 0x1fffffu) << 11);
             }
             qn += __popc(m);
             if (qn - qt >= 32) resolve(32);
@@ -374,8 +377,6 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
         }
         if (staging)
           while (head - tail >= 64) flush64();
-        if (!(last < xend)) break;
-        base = last + 1.0;
       }
     } else {
       // ---- dense block (pbar >= 1): every position is a candidate ----

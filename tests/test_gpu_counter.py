@@ -148,7 +148,7 @@ def test_kernel_shape_invariance(api, name, n):
     w = workloads.make(name, n)
     ws = api.make_weight_sequence(w)
     base = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
-    for cfg in (0, 1, 2, 3):
+    for cfg in (0, 1, 2, 3, 4):
         ws.device.set_kernel_shape(cfg)
         r = api.stream_range(ws, ws.sum_S, 0, n, 31, mode="counter", track_shift=3)
         assert (r.count, r.checksum) == (base.count, base.checksum), cfg
