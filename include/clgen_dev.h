@@ -139,6 +139,14 @@ int clgen_dev_warp_profile(clgen_dev_ctx* ctx, int launch, double* max_over_mean
 int clgen_dev_counter_plan_info(clgen_dev_ctx* ctx, int* classes, int64_t* blocks, int64_t* chunks,
                                 int* dense_blocks, double* class_eps);
 
+/* Statistical-test support for the counter stream: runs the generator over
+ * all sources for seeds seed, seed+1, ..., seed+trials-1 in ONE launch (each
+ * trial is exactly clgen_dev_stream_range / generate_range with that seed)
+ * and counts every edge (u, v) in counts[u * n + v] (uint32, n*n entries,
+ * host or device; n <= 4096).  The per-pair frequencies are the law check of
+ * acceptance.cpp:80-124. */
+int clgen_dev_pair_trials(clgen_dev_ctx* ctx, double S, uint64_t seed, int64_t trials, uint32_t* counts);
+
 /* Count pass only: per-source edge counts (int32, hi-lo entries, host or device). */
 int clgen_dev_edge_counts(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t hi, uint64_t seed,
                           int32_t* counts, int64_t* total, int64_t* n_flagged);

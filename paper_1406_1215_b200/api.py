@@ -359,6 +359,16 @@ def stream_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
     return StreamResult(cnt.value, cks.value, nfl.value, degree)
 
 
+def pair_trials(ws: WeightSequence, S: float, seed: int, trials: int) -> np.ndarray:
+    """Counter stream over all sources for seeds seed..seed+trials-1 in one
+    launch; returns uint32[n, n] per-pair edge counts (n <= 4096)."""
+    n = ws.size()
+    out = np.zeros((n, n), np.uint32)
+    check(_lib.lib().clgen_dev_pair_trials(ws.device.handle, S, seed & 0xFFFFFFFFFFFFFFFF, int(trials),
+                                           out.ctypes.data))
+    return out
+
+
 def plan_ucp(ws: WeightSequence, P: int, with_costs: bool = False):
     """Level-1 UCP on the device, bit-identical to plan_ucp_oracle(ws, P)
     (partition.cpp:159-203).  Returns int64[P+1] boundaries, plus the

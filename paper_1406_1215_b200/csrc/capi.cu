@@ -146,8 +146,8 @@ struct clgen_dev_ctx {
   double cls_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
   double chunk_cand = env_double("CLGEN_CTR_CHUNK", 32768.0);
   int blk_shape = -1;  // clgen_dev_set_kernel_shape (-1: CLGEN_BLK_SHAPE / default)
-  int blk_grid[3][5] = {};
-  size_t blk_smem[3][5] = {};
+  int blk_grid[4][5] = {};
+  size_t blk_smem[4][5] = {};
   // optional per-warp busy intervals of the sampler kernels
   bool warp_prof = false;
   DevBuf prof;
@@ -525,6 +525,8 @@ clg::BlkArgs blk_args(clgen_dev_ctx* c, double S, uint64_t seed) {
   a.total_chunks = c->chunk_total.as<int64_t>();
   a.queue = &c->sc->queue;
   a.seed_mix = clg::mix64(seed ^ 0x636c67656e626c6bULL);  // "clgenblk" domain tag
+  a.seed = seed;
+  a.trials = 1;
   a.logtab = c->logtab;
   a.overflow = &c->sc->overflow;
   a.fold_out = c->sc->fold;
@@ -570,7 +572,7 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
   static const int env_e = [] {
     const char* e = std::getenv("CLGEN_BLK_E");  // candidates per lane per loop iteration (unroll; same stream)
     const int v = e ? std::atoi(e) : kBlkE;
-    return v == 2 ? 2 : (v == 1 ? 1 : kBlkE);
+    return v == 2 ? 2 : kBlkE;
   }();
   auto by_shape = [&](auto e_tag) -> int {
     constexpr int EE = decltype(e_tag)::value;
@@ -582,9 +584,12 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
       default: return launch(clg::blk_kernel<MODE, EE, 256, 4>, 256);
     }
   };
-  if (env_e == 1) return by_shape(std::integral_constant<int, 1>{});
-  if (env_e == 2) return by_shape(std::integral_constant<int, 2>{});
-  return by_shape(std::integral_constant<int, kBlkE>{});
+  if constexpr (MODE == clg::kWalkPairs) {
+    return launch(clg::blk_kernel<MODE, kBlkE, 256, 4>, 256);  // test support: one shape
+  } else {
+    if (env_e == 2) return by_shape(std::integral_constant<int, 2>{});
+    return by_shape(std::integral_constant<int, kBlkE>{});
+  }
 }
 
 __global__ void pairs_to_keys_kernel(const uint2* __restrict__ p, int64_t m, unsigned long long* keys) {
@@ -1225,6 +1230,31 @@ int clgen_dev_generate_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi,
   if (n_flagged) *n_flagged = 0;
   c->last_flagged = 0;
   return materialise_ctr(c, S, lo, hi, seed, pairs, cap, count);
+}
+
+int clgen_dev_pair_trials(clgen_dev_ctx* c, double S, uint64_t seed, int64_t trials, uint32_t* counts) {
+  if (!c || !counts || trials < 0) return fail(CLGEN_EINVAL, "pair_trials: bad argument");
+  const int64_t n = c->n;
+  if (n > 4096) return fail(CLGEN_EINVAL, "pair_trials: n must be <= 4096 (n*n counters)");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const size_t bytes = static_cast<size_t>(n) * n * sizeof(uint32_t);
+  const bool dev_out = is_device_ptr(counts);
+  CUDA_TRY(c->probe.ensure(bytes > 0 ? bytes : 8));
+  uint32_t* d_counts = dev_out ? counts : c->probe.as<uint32_t>();
+  if (bytes) CUDA_TRY(cudaMemsetAsync(d_counts, 0, bytes, c->stream));
+  if ((rc = reset_scalars(c, 0))) return rc;
+  if (n >= 2 && S > 0.0 && trials > 0) {
+    if ((rc = ensure_blocks(c, S))) return rc;
+    if ((rc = ensure_range(c, 0, n))) return rc;
+    clg::BlkArgs a = blk_args(c, S, seed);
+    a.trials = trials;
+    a.pair_counts = d_counts;
+    a.n = static_cast<uint32_t>(n);
+    if ((rc = launch_blk<clg::kWalkPairs>(c, a))) return rc;
+  }
+  if (!dev_out && bytes) CUDA_TRY(cudaMemcpyAsync(counts, d_counts, bytes, cudaMemcpyDeviceToHost, c->stream));
+  return fetch_scalars(c);
 }
 
 int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chunk_cand) {

@@ -88,6 +88,12 @@ struct BlkArgs {
   unsigned long long* fold_out;
   unsigned long long* overflow;
   WarpProf prof;
+  // kWalkPairs: seeds seed..seed+trials-1 in one launch (launch chunk q of
+  // trial t is claim t * total + q), edges counted in pair_counts[u * n + v]
+  uint64_t seed;
+  int64_t trials;
+  uint32_t* pair_counts;
+  uint32_t n;
 };
 
 // E = -log(U) ~ Exp(1) by inversion, U = ((x >> 12) + 1/2) 2^-52 in (0,1)
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     smask = (1u << sl) - 1u;
     seg = a.ring + ((static_cast<unsigned long long>(gw) << sl) & a.ring_mask);
   }
-  constexpr bool staging = MODE != kWalkCount;  // fold: every edge is staged (fold + ring at flush)
+  constexpr bool staging = MODE == kWalkWrite || MODE == kWalkFold;  // fold: every edge is staged (fold + ring at flush)
   uint32_t head = 0, tail = 0;  // stage counters (warp-uniform)
   uint64_t checksum = 0;
   uint64_t wedges = 0;          // edges of this warp
@@ -276,6 +282,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   uint32_t cw = 0;  // edges of the current chunk (warp-uniform)
   // one candidate slot per lane: stage the accepted pairs
   auto emit1 = [&](bool acc, uint32_t u, uint32_t v) {
+    if (MODE == kWalkPairs && acc) atomicAdd(&a.pair_counts[static_cast<uint64_t>(u) * a.n + v], 1u);
     const unsigned b = __ballot_sync(CLG_FULL, acc);
     const uint32_t nb = __popc(b);
     if (staging) {
@@ -288,8 +295,16 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   for (;;) {
     unsigned long long qq = 0;
     if (lane == 0) qq = atomicAdd(a.queue, 1ull);
-    const int64_t q = static_cast<int64_t>(__shfl_sync(CLG_FULL, qq, 0));
-    if (q >= total) break;
+    int64_t q = static_cast<int64_t>(__shfl_sync(CLG_FULL, qq, 0));
+    uint64_t seed_mix = a.seed_mix;
+    if (MODE == kWalkPairs) {
+      if (total == 0 || q >= total * a.trials) break;
+      const int64_t t = q / total;
+      q -= t * total;
+      seed_mix = mix64((a.seed + static_cast<uint64_t>(t)) ^ 0x636c67656e626c6bULL);  // as blk_args
+    } else if (q >= total) {
+      break;
+    }
     const uint32_t b = __ldg(a.chunk_block + q);
     const BlockDesc d = a.blocks[b];
     const BlockRange r = a.ranges[b];
@@ -300,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     const double xend = static_cast<double>(x1);
     // a chunk cut by the launch's source range emits only the rows inside it
     const bool partial = r.x_lo > x0 || r.x_hi < x1;
-    const uint64_t key = mix64(a.seed_mix ^ (static_cast<uint64_t>(b) | (static_cast<uint64_t>(c) << 20)));
+    const uint64_t key = mix64(seed_mix ^ (static_cast<uint64_t>(b) | (static_cast<uint64_t>(c) << 20)));
     rng.seed_key(key + 0x632be59bd9b4e019ULL * static_cast<uint64_t>(lane + 1));
     __syncwarp();
     if (lane == 0) {

@@ -13,7 +13,8 @@
 
 namespace clg {
 
-enum WalkMode : int { kWalkCount = 0, kWalkWrite = 1, kWalkFold = 2 };
+// kWalkPairs (counter stream only): many seeds per launch, per-pair edge counts (statistical tests)
+enum WalkMode : int { kWalkCount = 0, kWalkWrite = 1, kWalkFold = 2, kWalkPairs = 3 };
 
 struct RefWalkArgs {
   const double* __restrict__ w;  // non-increasing weights, n entries
