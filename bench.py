@@ -284,13 +284,23 @@ def run_ours(args):
     import torch
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("CLGEN_DIST_BACKEND", "nccl")  # gloo: multi-rank test on one GPU
         if backend == "nccl":
+            # NCCL's own init log names the communicator size ("nranks")
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size()}
+        if backend == "nccl":
+            v = torch.cuda.nccl.version()
+            comm["nccl_version"] = ".".join(map(str, v)) if isinstance(v, tuple) else v
+        print(f"[clgen] rank {rank}: {comm['backend']} communicator nranks={comm['nranks']}",
+              file=sys.stderr, flush=True)
     import inputs
     from paper_1406_1215_b200 import api, runtime
 
@@ -368,6 +378,12 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     clk = clocks.stop()
+
+    # the level-1 plan's per-rank device phases for an 8-GPU run, timed rank
+    # by rank on this GPU (untimed for `value`; N = 1 plans trivially)
+    plan8 = None
+    if world == 1 and not materialise:
+        plan8 = runtime.plan_phase_times(dev, n, S, 8)
 
     # level-2 balance evidence: one extra untimed step with per-warp busy intervals
     dev.set_warp_profile(True)
@@ -448,6 +464,8 @@ def run_ours(args):
             # sources whose skip ratio fell in the libm-ambiguity band (reference
             # stream only); the counter stream has none by construction
             "n_flagged": flags[0],
+            "comm": comm,
+            "plan_g8_on_one_gpu": plan8,
             "load_balance": {
                 "per_launch_warp_busy": [
                     {"max_over_mean": round(p["max_over_mean"], 4), "mean_ms": round(p["mean_ms"], 3),

@@ -18,9 +18,18 @@
 //   serial_cl               edge_skip.hpp:63      serial_cl
 //   plan_ucp_oracle         partition.hpp:56      plan_ucp_oracle (device, bit-identical)
 //   PartitionPlan           partition.hpp:20-31   PartitionPlan (ucp fields)
+//   generate / GenConfig / GenReport  runtime.hpp:16-47, runtime.cpp:93-138
+//                                                 generate over clgen_spmd_generate
+//                                                 (one host thread per GPU, NCCL)
+//
+// EdgeSink gains one additive member, emit_bulk: the device
+// hands a sink a whole materialised run at once; EdgeVector appends it,
+// EdgeCounter only advances its count, any other sink still sees on_edge per
+// edge.
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <numeric>
@@ -65,8 +74,24 @@ struct WeightSequence {
   double sum_S = 0.0;               // blocked_sum(weights), computed on the device
   std::vector<node_t> orig_labels;  // sorted position -> original input label
   std::shared_ptr<Device> device;   // owns the device copy of the weights
+  // host-side sizing aid (lazily built): expected edges of sources [0, u)
+  // in the suffix form of node_costs_sequential (cost.cpp:62-77) minus the 1
+  mutable std::vector<double> expected_prefix;
 
   node_t size() const { return static_cast<node_t>(weights.size()); }
+  double expected_edges(node_t lo, node_t hi) const {
+    if (expected_prefix.empty()) {
+      expected_prefix.assign(weights.size() + 1, 0.0);
+      double suffix = 0.0;
+      std::vector<double> e(weights.size(), 0.0);
+      for (size_t u = weights.size(); u-- > 0;) {
+        e[u] = sum_S > 0.0 ? weights[u] / sum_S * suffix : 0.0;
+        suffix += weights[u];
+      }
+      for (size_t u = 0; u < weights.size(); ++u) expected_prefix[u + 1] = expected_prefix[u] + e[u];
+    }
+    return expected_prefix[static_cast<size_t>(hi)] - expected_prefix[static_cast<size_t>(lo)];
+  }
 };
 
 enum class SortPolicy { require_sorted, sort_desc };
@@ -124,10 +149,18 @@ class EdgeSink {
     on_edge(e);
     ++count_;
   }
+  // k (u, v) uint32 pairs in emission order; count() advances by k
+  void emit_bulk(const std::uint32_t* pairs, std::int64_t k) {
+    on_bulk(pairs, k);
+    count_ += k;
+  }
   std::int64_t count() const { return count_; }
 
  private:
   virtual void on_edge(const Edge& e) = 0;
+  virtual void on_bulk(const std::uint32_t* pairs, std::int64_t k) {
+    for (std::int64_t i = 0; i < k; ++i) on_edge(Edge{pairs[2 * i], pairs[2 * i + 1]});
+  }
   std::int64_t count_ = 0;
 };
 
@@ -137,25 +170,36 @@ class EdgeVector final : public EdgeSink {
 
  private:
   void on_edge(const Edge& e) override { edges.push_back(e); }
+  void on_bulk(const std::uint32_t* pairs, std::int64_t k) override {
+    edges.reserve(edges.size() + static_cast<size_t>(k));
+    for (std::int64_t i = 0; i < k; ++i) edges.push_back(Edge{pairs[2 * i], pairs[2 * i + 1]});
+  }
 };
 
 class EdgeCounter final : public EdgeSink {
  private:
   void on_edge(const Edge&) override {}
+  void on_bulk(const std::uint32_t*, std::int64_t) override {}
 };
 
 namespace detail {
-// Materialise on the device (uint32 pairs, reference emission order), then
-// feed the sink edge by edge so EdgeSink::count() advances as in the
-// reference.  Returns the emitted count.
+// Materialise on the device (uint32 pairs, reference emission order) in ONE
+// generation call sized from the expected edge count (+6 sigma), then hand
+// the run to the sink in bulk.  Only if the realised count exceeds that
+// capacity (CLGEN_ERANGE, with the exact count) is the call repeated.
 template <class Gen>
-std::int64_t run(Gen&& gen, EdgeSink& sink) {
+std::int64_t run(Gen&& gen, double expected, EdgeSink& sink) {
+  std::int64_t cap = static_cast<std::int64_t>(expected * 1.01 + 6.0 * std::sqrt(expected + 1.0)) + 4096;
+  std::vector<std::uint32_t> pairs(static_cast<size_t>(2 * cap));
   std::int64_t count = 0, flagged = 0;
-  int rc = gen(nullptr, 0, &count, &flagged);  // count pass sizes the buffer
-  if (rc != CLGEN_OK && rc != CLGEN_ERANGE) check(rc);
-  std::vector<std::uint32_t> pairs(static_cast<size_t>(2 * std::max<std::int64_t>(count, 1)));
-  if (count > 0) check(gen(pairs.data(), count, &count, &flagged));
-  for (std::int64_t i = 0; i < count; ++i) sink.emit(Edge{pairs[2 * i], pairs[2 * i + 1]});
+  int rc = gen(pairs.data(), cap, &count, &flagged);
+  if (rc == CLGEN_ERANGE) {
+    cap = count;
+    pairs.assign(static_cast<size_t>(2 * std::max<std::int64_t>(cap, 1)), 0u);
+    rc = gen(pairs.data(), cap, &count, &flagged);
+  }
+  check(rc);
+  sink.emit_bulk(pairs.data(), count);
   return count;
 }
 }  // namespace detail
@@ -163,22 +207,26 @@ std::int64_t run(Gen&& gen, EdgeSink& sink) {
 // edge_skip.cpp:60-66
 inline std::int64_t create_edges_range(const WeightSequence& ws, double S, node_t lo, node_t hi,
                                        std::uint64_t seed, EdgeSink& sink) {
+  const double e = (lo >= 0 && hi <= ws.size() && lo <= hi) ? ws.expected_edges(lo, hi) : 0.0;
   return detail::run(
       [&](std::uint32_t* p, std::int64_t cap, std::int64_t* cnt, std::int64_t* fl) {
         return clgen_dev_create_edges_range(ws.device->get(), S, lo, hi, seed, p, cap, cnt, fl);
       },
-      sink);
+      e, sink);
 }
 
 // edge_skip.cpp:50-58
 inline std::int64_t create_edges(const WeightSequence& ws, double S, std::span<const node_t> sources,
                                  std::uint64_t seed, EdgeSink& sink) {
+  double e = 0.0;
+  for (node_t u : sources)
+    if (u >= 0 && u < ws.size()) e += ws.expected_edges(u, u + 1);
   return detail::run(
       [&](std::uint32_t* p, std::int64_t cap, std::int64_t* cnt, std::int64_t* fl) {
         return clgen_dev_create_edges(ws.device->get(), S, sources.data(),
                                       static_cast<int64_t>(sources.size()), seed, p, cap, cnt, fl);
       },
-      sink);
+      e, sink);
 }
 
 // edge_skip.cpp:68-70
@@ -210,7 +258,7 @@ inline PartitionPlan plan_ucp_oracle(const WeightSequence& ws, int P) {
 // ---- streaming fold (no reference counterpart) -------------------------------
 struct StreamFold {
   std::int64_t edges = 0;
-  std::uint64_t checksum = 0;  // sum of mix64((u<<32)|v) mod 2^64
+  std::uint64_t checksum = 0;  // sum of edge_hash(u, v) mod 2^64 (clgen_dev.h)
   std::int64_t flagged = 0;
 };
 
@@ -221,6 +269,66 @@ inline StreamFold stream_range(const WeightSequence& ws, double S, node_t lo, no
                                counter_stream ? CLGEN_STREAM_COUNTER : CLGEN_STREAM_REFERENCE, 0,
                                nullptr, 0, nullptr, 0, &f.edges, &f.checksum, &f.flagged));
   return f;
+}
+
+// ---- whole runs (runtime.hpp:16-47, runtime.cpp:93-138) ----------------------
+// GenConfig / GenReport keep the reference's meaning for the fields that apply
+// to the device path: procs = GPUs (one host thread each), the UCP scheme,
+// count-only generation (the reference's empty out_dir).
+struct GenConfig {
+  int procs = 1;
+  std::uint64_t seed = 1;
+  std::vector<int> devices;      // default: 0 .. procs-1
+  bool counter_stream = true;    // false: the bit-exact reference stream
+};
+
+struct RankReport {
+  int rank = 0;
+  node_t n_lo = 0, n_hi = 0;
+  std::int64_t edges = 0;
+  double gen_wall_ms = 0.0;  // the timed generation section (runtime.cpp:74-86)
+  double kernel_ms = 0.0;    // its sampler kernel on the device
+};
+
+struct GenReport {
+  int procs = 1;
+  std::vector<node_t> boundaries;
+  std::vector<RankReport> ranks;
+  std::int64_t total_edges = 0;
+  std::uint64_t checksum = 0;
+  std::int64_t flagged = 0;
+  double sum_S = 0.0, sum_check = 0.0;
+  double wall_ms = 0.0, plan_ms = 0.0;
+  int nccl_version = 0;  // 0: in-process host communicator (ranks sharing a GPU)
+};
+
+inline GenReport generate(const WeightSequence& ws, const GenConfig& cfg) {
+  if (cfg.procs < 1) throw error("generate: procs must be >= 1");
+  std::vector<int> devs = cfg.devices;
+  if (devs.empty())
+    for (int g = 0; g < cfg.procs; ++g) devs.push_back(g);
+  if (static_cast<int>(devs.size()) != cfg.procs) throw error("generate: one device per rank");
+  GenReport rep;
+  rep.procs = cfg.procs;
+  rep.boundaries.assign(static_cast<size_t>(cfg.procs) + 1, 0);
+  std::vector<std::int64_t> edges(static_cast<size_t>(cfg.procs));
+  std::vector<double> gen(static_cast<size_t>(cfg.procs)), kern(static_cast<size_t>(cfg.procs));
+  clgen_spmd_report r{};
+  check(clgen_spmd_generate(devs.data(), cfg.procs, ws.weights.data(), ws.size(), cfg.seed,
+                            cfg.counter_stream ? CLGEN_STREAM_COUNTER : CLGEN_STREAM_REFERENCE,
+                            rep.boundaries.data(), edges.data(), gen.data(), kern.data(), &r));
+  for (int g = 0; g < cfg.procs; ++g)
+    rep.ranks.push_back(RankReport{g, rep.boundaries[static_cast<size_t>(g)], rep.boundaries[static_cast<size_t>(g) + 1],
+                                   edges[static_cast<size_t>(g)], gen[static_cast<size_t>(g)], kern[static_cast<size_t>(g)]});
+  rep.total_edges = r.total_edges;
+  rep.checksum = r.checksum;
+  rep.flagged = r.n_flagged;
+  rep.sum_S = r.S;
+  rep.sum_check = r.S_check;
+  rep.wall_ms = r.wall_ms;
+  rep.plan_ms = r.plan_ms;
+  rep.nccl_version = r.nccl_version;
+  return rep;
 }
 
 }  // namespace clgen_b200

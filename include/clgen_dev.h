@@ -229,6 +229,40 @@ int clgen_dev_edge_degrees(clgen_dev_ctx* ctx, const uint32_t* pairs, int64_t m,
 /* Ids of the sources flagged by the last generation call (up to cap). */
 int clgen_dev_flagged_nodes(clgen_dev_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
 
+/*
+ * Whole-run SPMD entry, the analogue of generate(ws, GenConfig)
+ * (runtime.cpp:93-138) over run_spmd (comm.cpp:204-227): G host threads, one
+ * per GPU devices[g], each with its own context.  Every rank copies the
+ * (non-increasing) weights w[0..n), computes S itself, runs the level-1 UCP
+ * plan (partition.cpp:107-157) with the reference's collectives on NCCL
+ * (ncclCommInitAll over the devices; all-gathers of block weights / block
+ * costs folded in rank order on the host, MIN all-reduce of the found
+ * boundaries), then streams its partition [b_g, b_{g+1}) with the fold
+ * (count + checksum; stream_mode as in clgen_dev_stream_range) and the
+ * totals are summed with one all-reduce.  Ranks that share a device (tests
+ * on a one-GPU box, or CLGEN_SPMD_COMM=host) use an in-process host
+ * communicator with the same semantics instead of NCCL.
+ * Outputs: boundaries[G+1] (== plan_ucp_oracle(ws, G)); per rank (optional,
+ * G entries each): edges, host wall ms and sampler-kernel ms of the timed
+ * generation section; and the report below.  Errors: the lowest failing
+ * rank's message, prefixed "rank g: ".
+ */
+typedef struct {
+  int G;
+  double S;            /* canonical blocked_sum, every rank's */
+  double S_check;      /* rank-ordered fold of the block weights (runtime.cpp:55-58) */
+  int64_t total_edges;
+  uint64_t checksum;   /* sum over all edges of edge_hash(u, v) mod 2^64 */
+  int64_t n_flagged;
+  double wall_ms;      /* whole SPMD section */
+  double plan_ms;      /* max over ranks of the plan (phases + collectives) */
+  int nccl_version;    /* 0: the in-process host communicator carried the collectives */
+} clgen_spmd_report;
+
+int clgen_spmd_generate(const int* devices, int G, const double* w, int64_t n, uint64_t seed,
+                        int stream_mode, int64_t* boundaries, int64_t* rank_edges,
+                        double* rank_gen_ms, double* rank_kernel_ms, clgen_spmd_report* report);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,7 @@ def _declare(L):
     L.clgen_dev_edge_degrees.argtypes = [_vp, _vp, _i64, _vp]
     L.clgen_dev_generate_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, _vp, _i64,
                                            _i64p, _i64p]
+    L.clgen_spmd_generate.argtypes = [_vp, C.c_int, _vp, _i64, _u64, C.c_int, _vp, _vp, _vp, _vp, _vp]
     L.clgen_dev_pair_trials.argtypes = [_vp, C.c_double, _u64, _i64, _vp]
     L.clgen_dev_set_counter_params.argtypes = [_vp, C.c_double, C.c_double]
     L.clgen_dev_set_fast_math.argtypes = [_vp, C.c_int]
@@ -101,9 +102,9 @@ EXPORTS = (
     "clgen_dev_flagged_nodes", "clgen_dev_plan_ucp", "clgen_dev_plan_block_weight",
     "clgen_dev_plan_block_costs", "clgen_dev_plan_block_boundaries", "clgen_dev_generate_range",
     "clgen_dev_set_counter_params", "clgen_dev_pair_trials", "clgen_dev_counter_plan_info", "clgen_dev_set_fast_math",
-"clgen_dev_set_warp_profile", "clgen_dev_set_kernel_shape", "clgen_dev_warp_profile",
+    "clgen_dev_set_warp_profile", "clgen_dev_set_kernel_shape", "clgen_dev_warp_profile",
     "clgen_dev_warp_profile_launches", "clgen_dev_write_edges",
-    "clgen_dev_fidelity", "clgen_dev_edge_degrees",
+    "clgen_dev_fidelity", "clgen_dev_edge_degrees", "clgen_spmd_generate",
 )
 
 

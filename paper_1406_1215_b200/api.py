@@ -369,6 +369,34 @@ def pair_trials(ws: WeightSequence, S: float, seed: int, trials: int) -> np.ndar
     return out
 
 
+class _SpmdReport(C.Structure):
+    _fields_ = [("G", C.c_int), ("S", C.c_double), ("S_check", C.c_double),
+                ("total_edges", C.c_int64), ("checksum", C.c_uint64), ("n_flagged", C.c_int64),
+                ("wall_ms", C.c_double), ("plan_ms", C.c_double), ("nccl_version", C.c_int)]
+
+
+def spmd_generate(weights, devices, seed: int, mode: str = "counter") -> dict:
+    """generate(ws, GenConfig) over one host thread per GPU (runtime.cpp:93-138,
+    comm.cpp:204-227): level-1 UCP plan with NCCL collectives, each rank
+    streams its partition; returns the plan, per-rank counts/times and totals."""
+    w = np.ascontiguousarray(weights, np.float64).reshape(-1)
+    devs = np.ascontiguousarray(devices, np.int32).reshape(-1)
+    G = int(devs.size)
+    sm = {"reference": STREAM_REFERENCE, "counter": STREAM_COUNTER}[mode]
+    b = np.zeros(G + 1, np.int64)
+    edges = np.zeros(G, np.int64)
+    gen_ms = np.zeros(G)
+    kern_ms = np.zeros(G)
+    rep = _SpmdReport()
+    check(_lib.lib().clgen_spmd_generate(devs.ctypes.data, G, w.ctypes.data if w.size else None, w.size,
+                                         seed & 0xFFFFFFFFFFFFFFFF, sm, b.ctypes.data, edges.ctypes.data,
+                                         gen_ms.ctypes.data, kern_ms.ctypes.data, C.byref(rep)))
+    return {"boundaries": b, "rank_edges": edges, "rank_gen_ms": gen_ms, "rank_kernel_ms": kern_ms,
+            "G": rep.G, "S": rep.S, "S_check": rep.S_check, "total_edges": rep.total_edges,
+            "checksum": rep.checksum, "n_flagged": rep.n_flagged, "wall_ms": rep.wall_ms,
+            "plan_ms": rep.plan_ms, "nccl_version": rep.nccl_version}
+
+
 def plan_ucp(ws: WeightSequence, P: int, with_costs: bool = False):
     """Level-1 UCP on the device, bit-identical to plan_ucp_oracle(ws, P)
     (partition.cpp:159-203).  Returns int64[P+1] boundaries, plus the

@@ -113,6 +113,9 @@ double env_double(const char* name, double dflt) {
 
 }  // namespace
 
+// spmd.cu reports its (lowest failing rank's) error through the caller's slot
+int clgen_internal_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+
 struct clgen_dev_ctx {
   int device = 0;
   int num_sms = 148;

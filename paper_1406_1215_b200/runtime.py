@@ -58,6 +58,41 @@ def plan(ws: api.WeightSequence, world: int, rank: int) -> np.ndarray:
     return _plan.plan_ucp_distributed(ws, world, rank)
 
 
+def plan_phase_times(dev, n: int, S: float, G: int) -> dict:
+    """The level-1 plan's three per-rank device phases for G ranks
+    (partition.cpp:115-154: block weight, block_cumulative, boundaries), run
+    rank after rank on this one GPU and host-timed (each phase returns a
+    scalar, i.e. synchronises).  Max over ranks of the per-rank sum is the
+    device time each GPU of a G-GPU run spends planning (the NCCL
+    all-gathers / all-reduce between the phases carry 8-byte payloads and
+    are not included)."""
+    import time
+    from .plan import DevicePhases, fold_prefix
+    ph = DevicePhases(dev)
+    t_bw, t_bc, t_bd, bws, zs = [], [], [], [], []
+    for g in range(G):
+        t0 = time.perf_counter()
+        bws.append(ph.block_weight(G, g))
+        t_bw.append((time.perf_counter() - t0) * 1e3)
+    for g in range(G):
+        t0 = time.perf_counter()
+        zs.append(ph.block_costs(G, g, fold_prefix(bws, g), S))
+        t_bc.append((time.perf_counter() - t0) * 1e3)
+    z_bar = fold_prefix(zs, G) / G
+    found = []
+    for g in range(G):
+        t0 = time.perf_counter()
+        found.append(ph.block_boundaries(G, g, fold_prefix(zs, g), z_bar))
+        t_bd.append((time.perf_counter() - t0) * 1e3)
+    b = np.min(np.stack(found), axis=0)
+    b[0], b[G] = 0, n
+    per_rank = [a + c + d for a, c, d in zip(t_bw, t_bc, t_bd)]
+    return {"G": G, "block_weight_ms": [round(x, 3) for x in t_bw],
+            "block_costs_ms": [round(x, 3) for x in t_bc],
+            "boundaries_ms": [round(x, 3) for x in t_bd],
+            "per_rank_max_ms": round(max(per_rank), 3), "boundaries": b.tolist()}
+
+
 def expected_edges(w: np.ndarray, S: float, lo: int, hi: int) -> float:
     """Expected edges of sources [lo,hi) (unclamped, an upper bound of the
     clamped mean) plus a 6-sigma margin: capacity sizing only."""

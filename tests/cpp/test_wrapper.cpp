@@ -64,6 +64,26 @@ int main() {
   for (const Edge& e : a.edges) CHECK(e.u < e.v && e.v < big.size());
   const auto f = stream_range(big, big.sum_S, 0, big.size(), 42, false);
   CHECK(f.edges == a.count());
+  EdgeCounter counter;
+  CHECK(serial_cl(big, 42, counter) == a.count() && counter.count() == a.count());
+
+  // generate (runtime.cpp:93-138) over one host thread per rank: the plan is
+  // plan_ucp_oracle's and the union of the ranks' streams is serial_cl's
+  for (int procs : {1, 3}) {
+    GenConfig cfg;
+    cfg.procs = procs;
+    cfg.seed = 42;
+    cfg.devices.assign(static_cast<size_t>(procs), 0);  // one GPU: ranks share it
+    cfg.counter_stream = false;
+    const GenReport rep = generate(big, cfg);
+    CHECK(rep.boundaries == plan_ucp_oracle(big, procs).boundaries);
+    CHECK(rep.total_edges == a.count());
+    CHECK(rep.checksum == f.checksum);
+    CHECK(rep.sum_S == big.sum_S);
+    std::int64_t sum = 0;
+    for (const auto& r : rep.ranks) sum += r.edges;
+    CHECK(sum == rep.total_edges);
+  }
 
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

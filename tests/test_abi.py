@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "clgen_dev.h")
 
 def declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(clgen_dev_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(clgen_(?:dev|spmd)_\w+)\s*\(", src, re.M)))
 
 
 def lib_path():
@@ -26,6 +26,7 @@ def test_header_declares_entry_points():
     names = declared()
     assert "clgen_dev_create_edges_range" in names
     assert "clgen_dev_stream_range" in names
+    assert "clgen_spmd_generate" in names
     assert len(names) >= 10
 
 
@@ -35,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared():
         assert hasattr(lib, name), name
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
-    exported = set(re.findall(r"\b(clgen_dev_\w+)\b", out))
+    exported = set(re.findall(r"\b(clgen_(?:dev|spmd)_\w+)\b", out))
     assert set(declared()) <= exported
 
 
