@@ -394,6 +394,10 @@ def run_ours(args):
     # max over ranks of the device time; sum of edges
     ms_step = total_ms / args.steps
     per_gpu = [ms_step]
+    planned = None
+    if world > 1:  # planned cost per GPU (fill_partition_costs) beside the measured times
+        pc = api.fill_partition_costs(api.PartitionPlan("ucp", world, n, np.asarray(bounds)), ws)
+        planned = {"per_gpu_cost": pc.tolist(), "max_over_mean": float(pc.max() / pc.mean())}
     if world > 1:
         import torch.distributed as dist
         g = torch.zeros(world, dtype=torch.float64, device=runtime.comm_device(local))
@@ -472,6 +476,7 @@ def run_ours(args):
                      "max_ms": round(p["max_ms"], 3), "span_ms": round(p["span_ms"], 3),
                      "warps": p["warps"]} for p in wprof],
                 "per_gpu_ms": per_gpu,
+                "planned": planned,
                 "per_gpu_max_over_mean": max(per_gpu) / (sum(per_gpu) / len(per_gpu))},
             "clocks": clk,
         }

@@ -197,6 +197,26 @@ int clgen_dev_plan_block_costs(clgen_dev_ctx* ctx, int G, int g, double sigma_st
 int clgen_dev_plan_block_boundaries(clgen_dev_ctx* ctx, int G, int g, double z_offset,
                                     double z_bar, int64_t* found);
 
+/* Partition schemes (partition.hpp:15). */
+#define CLGEN_SCHEME_NAIVE 0
+#define CLGEN_SCHEME_UCP 1
+#define CLGEN_SCHEME_RRP 2
+
+/* node_costs_sequential (cost.cpp:62-77): the suffix-form per-node cost
+ * (w_u / S) * sum_{v>u} w_v + 1 with the suffix accumulated backward from
+ * 0.0, bit-identical (an exact reversed fold); costs: n doubles, host or
+ * device. */
+int clgen_dev_node_costs(clgen_dev_ctx* ctx, double* costs);
+/* fill_partition_costs (partition.cpp:205-222): per-partition expected cost,
+ * each a left fold from 0.0 of node_costs_sequential over the partition's
+ * nodes (consecutive [b_i, b_{i+1}) for naive/ucp, u = i mod P ascending for
+ * rrp), bit-identical.  boundaries: P+1 (host or device; ignored for rrp);
+ * per: P doubles (host). */
+int clgen_dev_partition_costs(clgen_dev_ctx* ctx, int scheme, int P, const int64_t* boundaries, double* per);
+/* expected_total_edges (weights.cpp:155-162): (S^2 - blocked_sum(w^2)) / (2S)
+ * with the canonical S, bit-identical; 0 when S <= 0. */
+int clgen_dev_expected_total_edges(clgen_dev_ctx* ctx, double* m);
+
 /*
  * Persist edges in the reference's formats (edge_io.cpp:72-88): binary
  * CLGEDGE1 (16-byte header, u64 count, u64 pairs) or text "u v" lines.

@@ -263,6 +263,8 @@ class _Ref:
         L.ref_fold_edges_range.argtypes = [vp, C.c_double, _i64, _i64, _u64, _i64p, _i64p, _u64p]
         L.ref_naive_pair_sampler.argtypes = [vp, _u64, _u32p, _i64, _i64p]
         L.ref_plan_ucp_oracle.argtypes = [vp, C.c_int, _i64p]
+        L.ref_node_costs_sequential.argtypes = [vp, _dp]
+        L.ref_fill_partition_costs.argtypes = [vp, C.c_int, C.c_int, _i64p, _dp]
         L.ref_plan_ucp_spmd.argtypes = [vp, C.c_int, _i64p]
         L.ref_global_cum_costs.argtypes = [vp, C.c_int, _dp, _dp, _dp]
         L.ref_generate_count.argtypes = [vp, C.c_int, C.c_int, _u64, _i64p, _dp, _dp, _i64p]
@@ -372,6 +374,18 @@ class _Ref:
         b = np.empty(max(P, 0) + 1, np.int64)
         self._check(self.lib.ref_plan_ucp_oracle(ws.h, P, _ptr(b, _i64p)))
         return b
+
+    def node_costs_sequential(self, ws: RefWS) -> np.ndarray:
+        out = np.empty(max(ws.n, 1), np.float64)
+        self._check(self.lib.ref_node_costs_sequential(ws.h, _ptr(out, _dp)))
+        return out[: ws.n]
+
+    def fill_partition_costs(self, ws: RefWS, scheme: str, P: int, boundaries=None) -> np.ndarray:
+        sch = {"naive": 0, "ucp": 1, "rrp": 2}[scheme]
+        b = np.ascontiguousarray(boundaries if boundaries is not None else np.zeros(P + 1), np.int64)
+        out = np.empty(P, np.float64)
+        self._check(self.lib.ref_fill_partition_costs(ws.h, sch, P, _ptr(b, _i64p), _ptr(out, _dp)))
+        return out
 
     def plan_ucp_spmd(self, ws: RefWS, P) -> np.ndarray:
         b = np.empty(P + 1, np.int64)

@@ -216,6 +216,28 @@ int ref_naive_pair_sampler(void* h, std::uint64_t seed, std::uint32_t* pairs, st
   });
 }
 
+int ref_node_costs_sequential(void* h, double* out) {
+  return guard([&] {
+    const auto c = node_costs_sequential(*static_cast<WeightSequence*>(h));
+    std::copy(c.begin(), c.end(), out);
+  });
+}
+
+// scheme: 0 naive, 1 ucp, 2 rrp (partition.hpp:15); boundaries unused for rrp
+int ref_fill_partition_costs(void* h, int scheme, int P, const std::int64_t* boundaries, double* out) {
+  return guard([&] {
+    const auto& ws = *static_cast<WeightSequence*>(h);
+    PartitionPlan plan;
+    plan.scheme = scheme == 2 ? Scheme::rrp : (scheme == 1 ? Scheme::ucp : Scheme::naive);
+    plan.procs = P;
+    plan.n = ws.size();
+    if (scheme == 2) plan.rrp_modulus = P;
+    else plan.boundaries.assign(boundaries, boundaries + P + 1);
+    fill_partition_costs(plan, ws);
+    std::copy(plan.per_partition_cost.begin(), plan.per_partition_cost.end(), out);
+  });
+}
+
 int ref_plan_ucp_oracle(void* h, int P, std::int64_t* boundaries) {
   return guard([&] {
     auto plan = plan_ucp_oracle(*static_cast<WeightSequence*>(h), P);

@@ -74,6 +74,9 @@ def _declare(L):
     L.clgen_dev_edge_degrees.argtypes = [_vp, _vp, _i64, _vp]
     L.clgen_dev_generate_range.argtypes = [_vp, C.c_double, _i64, _i64, _u64, C.c_int, _vp, _i64,
                                            _i64p, _i64p]
+    L.clgen_dev_node_costs.argtypes = [_vp, _vp]
+    L.clgen_dev_partition_costs.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
+    L.clgen_dev_expected_total_edges.argtypes = [_vp, _dp]
     L.clgen_spmd_generate.argtypes = [_vp, C.c_int, _vp, _i64, _u64, C.c_int, _vp, _vp, _vp, _vp, _vp]
     L.clgen_dev_pair_trials.argtypes = [_vp, C.c_double, _u64, _i64, _vp]
     L.clgen_dev_set_counter_params.argtypes = [_vp, C.c_double, C.c_double]
@@ -105,6 +108,7 @@ EXPORTS = (
     "clgen_dev_set_warp_profile", "clgen_dev_set_kernel_shape", "clgen_dev_warp_profile",
     "clgen_dev_warp_profile_launches", "clgen_dev_write_edges",
     "clgen_dev_fidelity", "clgen_dev_edge_degrees", "clgen_spmd_generate",
+    "clgen_dev_node_costs", "clgen_dev_partition_costs", "clgen_dev_expected_total_edges",
 )
 
 

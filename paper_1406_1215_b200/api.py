@@ -359,6 +359,33 @@ def stream_range(ws: WeightSequence, S: float, lo: int, hi: int, seed: int,
     return StreamResult(cnt.value, cks.value, nfl.value, degree)
 
 
+def node_costs_sequential(ws: WeightSequence) -> np.ndarray:
+    """cost.cpp:62-77 on the device, bit-identical (float64[n])."""
+    out = np.empty(max(ws.size(), 1), np.float64)
+    check(_lib.lib().clgen_dev_node_costs(ws.device.handle, out.ctypes.data))
+    return out[: ws.size()]
+
+
+def fill_partition_costs(plan: "PartitionPlan", ws: WeightSequence) -> np.ndarray:
+    """partition.cpp:205-222 on the device, bit-identical: per-partition
+    expected cost (float64[P]); also stored as plan.per_partition_cost."""
+    scheme = {"naive": 0, "ucp": 1, "rrp": 2}[plan.scheme]
+    per = np.zeros(plan.procs, np.float64)
+    b = None if plan.boundaries is None else np.ascontiguousarray(plan.boundaries, np.int64)
+    check(_lib.lib().clgen_dev_partition_costs(ws.device.handle, scheme, plan.procs,
+                                               b.ctypes.data if b is not None else None,
+                                               per.ctypes.data))
+    plan.per_partition_cost = per
+    return per
+
+
+def expected_total_edges(ws: WeightSequence) -> float:
+    """weights.cpp:155-162 on the device, bit-identical."""
+    out = C.c_double()
+    check(_lib.lib().clgen_dev_expected_total_edges(ws.device.handle, C.byref(out)))
+    return out.value
+
+
 def pair_trials(ws: WeightSequence, S: float, seed: int, trials: int) -> np.ndarray:
     """Counter stream over all sources for seeds seed..seed+trials-1 in one
     launch; returns uint32[n, n] per-pair edge counts (n <= 4096)."""
@@ -443,6 +470,7 @@ class PartitionPlan:
     procs: int
     n: int
     boundaries: np.ndarray | None = None
+    per_partition_cost: np.ndarray | None = None
 
     def partition_size(self, i: int) -> int:
         if i < 0 or i >= self.procs:

@@ -141,6 +141,7 @@ struct clgen_dev_ctx {
   DevBuf blocks, ranges, blk_cnt, blk_prefix, chunk_block, chunk_total, chunk_counts, chunk_offsets;
   DevBuf keys_a, keys_b, sort_tmp;  // materialised counter output: device sort by (u, v)
   DevBuf probe;                     // small scratch (fidelity histograms)
+  DevBuf costs;                     // node_costs_sequential (suffix-form costs)
   clg::ClassPlan plan_host{};
   bool cls_valid = false;
   bool blk_valid = false;
@@ -322,7 +323,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // Folds x[0..m) left to right from s0 exactly as a sequential FP64 loop
 // would; *final_host receives s_m.  out_mode/out/w/S per clg::FoldOut.
 int run_fold(clgen_dev_ctx* c, const double* x, int64_t m, double s0, int out_mode, double* out,
-             const double* w, double S, double* final_host) {
+             const double* w, double S, double* final_host, int64_t stride = 1, int reverse = 0) {
   if (m == 0) {
     *final_host = s0;
     return CLGEN_OK;
@@ -348,6 +349,8 @@ int run_fold(clgen_dev_ctx* c, const double* x, int64_t m, double s0, int out_mo
   a.out = out;
   a.w = w;
   a.S = S;
+  a.stride = stride;
+  a.reverse = reverse;
   const unsigned g = static_cast<unsigned>(T);
   clg::fold_tile_sums_kernel<<<g, clg::kFoldThreads, 0, c->stream>>>(a);
   clg::fold_approx_prefix_kernel<<<1, 1024, 0, c->stream>>>(a, T);
@@ -894,7 +897,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   c->foldtmp.release();
   c->cum.release();
   c->found.release();
-  for (DevBuf* d : {&c->cls_thr, &c->cls_bounds, &c->cls_start, &c->cls_wfirst, &c->cls_wlast, &c->cls_plan,
+  for (DevBuf* d : {&c->costs, &c->cls_thr, &c->cls_bounds, &c->cls_start, &c->cls_wfirst, &c->cls_wlast, &c->cls_plan,
                     &c->blocks, &c->ranges, &c->blk_cnt, &c->blk_prefix, &c->chunk_block, &c->chunk_total,
                     &c->chunk_counts, &c->chunk_offsets, &c->keys_a, &c->keys_b, &c->sort_tmp})
     d->release();
@@ -1233,6 +1236,95 @@ int clgen_dev_generate_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi,
   if (n_flagged) *n_flagged = 0;
   c->last_flagged = 0;
   return materialise_ctr(c, S, lo, hi, seed, pairs, cap, count);
+}
+
+// cost.cpp:62-77 on device data: suffixes accumulated backward from 0.0
+// (a reversed exact fold), costs[u] = (w_u / S) * suffix_u + 1; S <= 0: all 1.
+int node_costs_dev(clgen_dev_ctx* c, double** d_costs) {
+  const int64_t n = c->n;
+  CUDA_TRY(c->costs.ensure((n > 0 ? n : 1) * sizeof(double)));
+  *d_costs = c->costs.as<double>();
+  if (n == 0) return CLGEN_OK;
+  double S;
+  int rc = blocked_sum_impl(c, c->w, n, &S);
+  if (rc) return rc;
+  if (!(S > 0.0)) {
+    clg::fill_f64_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(*d_costs, 0, n, 1.0);
+    ++c->launches;
+    CUDA_TRY(cudaGetLastError());
+    return CLGEN_OK;
+  }
+  double total;
+  return run_fold(c, c->w, n, 0.0, clg::kFoldSuffixCost, *d_costs, nullptr, S, &total, 1, 1);
+}
+
+int clgen_dev_node_costs(clgen_dev_ctx* c, double* costs) {
+  if (!c || (c->n > 0 && !costs)) return fail(CLGEN_EINVAL, "node_costs: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  double* d = nullptr;
+  if ((rc = node_costs_dev(c, &d))) return rc;
+  if (c->n > 0) CUDA_TRY(cudaMemcpyAsync(costs, d, c->n * sizeof(double), cudaMemcpyDefault, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
+// partition.cpp:205-222: per-partition sums of the suffix-form costs, each a
+// left fold from 0.0 over the partition's nodes in ascending order.
+int clgen_dev_partition_costs(clgen_dev_ctx* c, int scheme, int P, const int64_t* boundaries, double* per) {
+  if (!c || P < 1 || !per || (scheme != CLGEN_SCHEME_RRP && !boundaries) || scheme < 0 || scheme > 2)
+    return fail(CLGEN_EINVAL, "fill_partition_costs: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  std::vector<int64_t> b;
+  if (scheme != CLGEN_SCHEME_RRP) {
+    b.resize(static_cast<size_t>(P) + 1);
+    CUDA_TRY(cudaMemcpy(b.data(), boundaries, b.size() * sizeof(int64_t), cudaMemcpyDefault));
+    for (int i = 0; i < P; ++i)
+      if (b[i] < 0 || b[i + 1] < b[i] || b[i + 1] > n) return fail(CLGEN_EINVAL, "fill_partition_costs: bad boundaries");
+  }
+  double* d = nullptr;
+  if ((rc = node_costs_dev(c, &d))) return rc;
+  for (int i = 0; i < P; ++i) {
+    double acc = 0.0;
+    if (scheme == CLGEN_SCHEME_RRP) {
+      const int64_t cnt = n > i ? (n - 1 - i) / P + 1 : 0;  // u = i, i + P, ...
+      if ((rc = run_fold(c, d + i, cnt, 0.0, clg::kFoldNone, nullptr, nullptr, 0.0, &acc, P, 0))) return rc;
+    } else {
+      if ((rc = run_fold(c, d + b[i], b[i + 1] - b[i], 0.0, clg::kFoldNone, nullptr, nullptr, 0.0, &acc))) return rc;
+    }
+    per[i] = acc;
+  }
+  return CLGEN_OK;
+}
+
+__global__ void squares_kernel(const double* __restrict__ w, int64_t n, double* out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __dmul_rn(w[i], w[i]);
+}
+
+// weights.cpp:155-162: (S^2 - blocked_sum(w^2)) / (2 S), S the canonical sum.
+int clgen_dev_expected_total_edges(clgen_dev_ctx* c, double* m) {
+  if (!c || !m) return fail(CLGEN_EINVAL, "expected_total_edges: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  double S;
+  if ((rc = blocked_sum_impl(c, c->w, n, &S))) return rc;
+  if (S <= 0.0) {
+    *m = 0.0;
+    return CLGEN_OK;
+  }
+  CUDA_TRY(c->costs.ensure(n * sizeof(double)));
+  squares_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(c->w, n, c->costs.as<double>());
+  ++c->launches;
+  CUDA_TRY(cudaGetLastError());
+  double sum_sq;
+  if ((rc = blocked_sum_impl(c, c->costs.as<double>(), n, &sum_sq))) return rc;
+  *m = (S * S - sum_sq) / (2.0 * S);
+  return CLGEN_OK;
 }
 
 int clgen_dev_pair_trials(clgen_dev_ctx* c, double S, uint64_t seed, int64_t trials, uint32_t* counts) {

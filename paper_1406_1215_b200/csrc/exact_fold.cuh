@@ -42,6 +42,7 @@ enum FoldOut : int {
   kFoldNone = 0,      // final value only
   kFoldInclusive = 1, // out[k] = s_{k+1}
   kFoldNodeCost = 2,  // out[k] = node_cost(x_k, s_k, S) (cost.cpp:8-13; s_k = sigma_u)
+  kFoldSuffixCost = 3,  // out[src(k)] = (x_k / S) * s_k + 1 (cost.cpp:62-77 with a reversed fold)
 };
 
 struct Fn {
@@ -157,9 +158,16 @@ struct FoldArgs {
   double* out;           // [m] (may alias x for kFoldInclusive)
   const double* w;       // kFoldNodeCost: x are the weights, S below
   double S;
+  int64_t stride;        // element k is x[src(k) * stride] (1: contiguous)
+  int reverse;           // src(k) = reverse ? m - 1 - k : k
 };
 
+__device__ __forceinline__ int64_t fold_src(const FoldArgs& a, int64_t k) { return a.reverse ? a.m - 1 - k : k; }
+__device__ __forceinline__ double fold_x(const FoldArgs& a, int64_t k) { return a.x[fold_src(a, k) * a.stride]; }
+__device__ __forceinline__ void fold_put(const FoldArgs& a, int64_t k, double v) { a.out[fold_src(a, k)] = v; }
+
 __device__ __forceinline__ double emit_value(const FoldArgs& a, double s_excl, double s_incl, double x) {
+  if (a.out_mode == kFoldSuffixCost) return __dadd_rn(__dmul_rn(__ddiv_rn(x, a.S), s_excl), 1.0);
   return a.out_mode == kFoldNodeCost ? node_cost_dev(x, s_excl, a.S) : s_incl;
 }
 
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_tile_sums_kernel(FoldArgs a
 #pragma unroll
   for (int i = 0; i < kFoldItems; ++i) {
     const int64_t k = base + i * kFoldThreads + threadIdx.x;
-    if (k < a.m) acc += a.x[k];
+    if (k < a.m) acc += fold_x(a, k);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CLG_FULL, acc, o);
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_tile_fun_kernel(FoldArgs a)
 #pragma unroll
   for (int i = 0; i < kFoldItems; ++i) {
     const int64_t k = my0 + i;
-    if (k < a.m) f = fn_compose(f, elem_fn(a.x[k], e, bad));
+    if (k < a.m) f = fn_compose(f, elem_fn(fold_x(a, k), e, bad));
   }
   if (bad) any_bad = 1;
   Fn tot;
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
       const int64_t b1 = b0 + kFoldTile < a.m ? b0 + kFoldTile : a.m;
       for (int64_t c = b0; c < b1; c += 32) {
         const int64_t k = c + lane;
-        const double xk = k < b1 ? a.x[k] : 0.0;
+        const double xk = k < b1 ? fold_x(a, k) : 0.0;
         double myout = 0.0;
         const int cnt = b1 - c < 32 ? static_cast<int>(b1 - c) : 32;
         for (int j = 0; j < cnt; ++j) {
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
           s = __dadd_rn(s, xj);
           if (lane == j) myout = emit_value(a, before, s, xj);
         }
-        if (a.out_mode != kFoldNone && k < b1) a.out[k] = myout;
+        if (a.out_mode != kFoldNone && k < b1) fold_put(a, k, myout);
       }
       binade_of(s, e, M);
     }
@@ -345,7 +353,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_emit_kernel(FoldArgs a) {
 #pragma unroll
   for (int i = 0; i < kFoldItems; ++i) {
     const int64_t k = my0 + i;
-    xs[i] = k < a.m ? a.x[k] : 0.0;
+    xs[i] = k < a.m ? fold_x(a, k) : 0.0;
     f = fn_compose(f, elem_fn(xs[i], e, bad));
   }
   Fn tot;
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_emit_kernel(FoldArgs a) {
     if (k >= a.m) break;
     const double before = from_binade(e, M);
     M = fn_apply(elem_fn(xs[i], e, bad), M);
-    a.out[k] = emit_value(a, before, from_binade(e, M), xs[i]);
+    fold_put(a, k, emit_value(a, before, from_binade(e, M), xs[i]));
   }
 }
 

@@ -87,10 +87,14 @@ def plan_phase_times(dev, n: int, S: float, G: int) -> dict:
     b = np.min(np.stack(found), axis=0)
     b[0], b[G] = 0, n
     per_rank = [a + c + d for a, c, d in zip(t_bw, t_bc, t_bd)]
+    # planned cost per GPU (fill_partition_costs, partition.cpp:205-222)
+    ws = api.WeightSequence(np.empty(0), S, None, dev)
+    planned = api.fill_partition_costs(api.PartitionPlan("ucp", G, n, b), ws)
     return {"G": G, "block_weight_ms": [round(x, 3) for x in t_bw],
             "block_costs_ms": [round(x, 3) for x in t_bc],
             "boundaries_ms": [round(x, 3) for x in t_bd],
-            "per_rank_max_ms": round(max(per_rank), 3), "boundaries": b.tolist()}
+            "per_rank_max_ms": round(max(per_rank), 3), "boundaries": b.tolist(),
+            "planned_cost_max_over_mean": float(planned.max() / planned.mean())}
 
 
 def expected_edges(w: np.ndarray, S: float, lo: int, hi: int) -> float:

@@ -182,3 +182,18 @@ def test_port_synth_matches_reference(port, ref):
     ws = ref.synth_powerlaw(5000, 2.1, 2.0, 1e5, 1)
     np.testing.assert_array_equal(ws.weights, port.synth_powerlaw(5000, 2.1, 2.0, 1e5, 1))
     assert ws.sum_S == port.blocked_sum(ws.weights)
+
+
+def test_input_synthesis_bit_identical_to_reference(ref):
+    """inputs (both bench arms' input preparation, libclgen_inputs.so) draws
+    synth_powerlaw's values bit for bit (weights.cpp:103-128; the reference
+    stable-sorts them, make_weight_sequence at :32-55) and synth_constant's
+    (:130-140) — for the C1/C3/C4/C5 parameter sets at n = 2e5."""
+    import inputs
+    for n, gamma, lo, hi, seed in ((200_000, 2.5, 10.0, 1000.0, 1), (200_000, 2.1, 2.0, 1e5, 1),
+                                   (200_000, 2.5, 1.0, 1000.0, 1), (200_000, 2.0, 1.0, 977.0, 3)):
+        got = inputs.powerlaw(n, gamma, lo, hi, seed)
+        exp = ref.synth_powerlaw(n, gamma, lo, hi, seed).weights
+        assert got.view(np.uint64).tolist() == exp.view(np.uint64).tolist()
+    c = ref.synth_constant(1000, 50.0)
+    assert np.array_equal(c.weights, np.full(1000, 50.0)) and c.sum_S == 50000.0
