@@ -109,7 +109,8 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
  * w_last inside a class; default 1/128, doubled until the classes fit 1024)
- * and the chunk size in expected candidates (0 = default 32768; range
+ * and the chunk size in expected candidates (0 = automatic: S / 2^19 clamped
+ * to [4096, 262144], a function of the weights only; explicit range
  * [256, 2^20]).  Both are part of the stream definition: changing them
  * changes the generated graph (not its law). */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double chunk_cand);
@@ -126,7 +127,7 @@ int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
 
 /* Counter-stream kernel shape (no reference counterpart; the edge set does
- * not depend on it): 256 threads x 2 / 3 / 4 (default) / 5 / 6 CTAs per SM
+ * not depend on it): 256 threads x 2 / 3 (default) / 4 / 5 / 6 CTAs per SM
  * for shape 0 / 1 / 2 / 3 / 4, -1 = CLGEN_BLK_SHAPE or the default.  flags must be
  * 0.  Used by the schedule-invariance tests. */
 int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int shape, int flags);

@@ -148,7 +148,7 @@ struct clgen_dev_ctx {
   double blk_S = 0.0;
   int64_t rng_lo = -1, rng_hi = -1;  // launch range the chunk tables hold
   double cls_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
-  double chunk_cand = env_double("CLGEN_CTR_CHUNK", 32768.0);
+  double chunk_cand = env_double("CLGEN_CTR_CHUNK", 0.0);  // 0: auto (auto_chunk_cand)
   int blk_shape = -1;  // clgen_dev_set_kernel_shape (-1: CLGEN_BLK_SHAPE / default)
   int blk_grid[4][5] = {};
   size_t blk_smem[4][5] = {};
@@ -164,6 +164,7 @@ struct clgen_dev_ctx {
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
   clg::LogTable* logtab = nullptr;  // device
+  clg::Log2Table* logtab2 = nullptr;  // device (counter stream: log2 table)
   // instrumentation: kernels launched by this context, and the duration of
   // the last dominant (sampler) kernel measured with events on the stream
   unsigned long long launches = 0;
@@ -438,6 +439,16 @@ int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, doubl
 // Class table of the weights (no host round trip) and block table for S (one
 // synchronisation: the host learns the class and chunk counts to size the
 // per-launch tables); both cached until the weights, S or the parameters change.
+// Automatic chunk size: S / 2 bounds the expected edge count; about 2^18
+// chunks per graph, between 4096 candidates (small graphs keep every warp
+// busy) and 262144 (8192 per lane: the lanes of a chunk end within ~2% of
+// one another).  A function of S only, so every GPU count and every cover of
+// the sources cuts the same chunks.
+double auto_chunk_cand(double S) {
+  const double c = std::floor(S * 0x1.0p-19);
+  return c < 4096.0 ? 4096.0 : (c > 262144.0 ? 262144.0 : c);
+}
+
 int ensure_blocks(clgen_dev_ctx* c, double S) {
   if (c->blk_valid && c->blk_S == S) return CLGEN_OK;
   const int kcap = clg::kClassCap;
@@ -467,7 +478,8 @@ int ensure_blocks(clgen_dev_ctx* c, double S) {
   {
     const dim3 blk(32, 8), grd((kcap + 31) / 32, (kcap + 7) / 8);
     clg::blk_desc_kernel<<<grd, blk, 0, c->stream>>>(c->cls_start.as<int64_t>(), c->cls_wfirst.as<double>(),
-                                                     c->cls_wlast.as<double>(), dp, S, c->chunk_cand,
+                                                     c->cls_wlast.as<double>(), dp, S,
+                                                     c->chunk_cand > 0.0 ? c->chunk_cand : auto_chunk_cand(S),
                                                      c->blocks.as<clg::BlockDesc>());
     ++c->launches;
     CUDA_TRY(cudaGetLastError());
@@ -533,7 +545,7 @@ clg::BlkArgs blk_args(clgen_dev_ctx* c, double S, uint64_t seed) {
   a.seed_mix = clg::mix64(seed ^ 0x636c67656e626c6bULL);  // "clgenblk" domain tag
   a.seed = seed;
   a.trials = 1;
-  a.logtab = c->logtab;
+  a.logtab = c->logtab2;
   a.overflow = &c->sc->overflow;
   a.fold_out = c->sc->fold;
   return a;
@@ -541,7 +553,7 @@ clg::BlkArgs blk_args(clgen_dev_ctx* c, double S, uint64_t seed) {
 
 // The counter-stream kernel: one persistent grid, warps claim chunks.  Block
 // shape (CLGEN_BLK_SHAPE or clgen_dev_set_kernel_shape): 256 threads x
-// 2 / 3 / 4 (default) / 5 / 6 CTAs per SM for shape 0 / 1 / 2 / 3 / 4; the
+// 2 / 3 (default: 80 registers, no spills) / 4 / 5 / 6 CTAs per SM for shape 0 / 1 / 2 / 3 / 4; the
 // edge set does not depend on it.
 constexpr int kBlkE = 4;  // candidates per lane per loop iteration (an unroll factor)
 
@@ -549,8 +561,8 @@ template <int MODE>
 int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
   static const int env_shape = [] {
     const char* e = std::getenv("CLGEN_BLK_SHAPE");
-    const int v = e ? std::atoi(e) : 2;
-    return v >= 0 && v <= 4 ? v : 2;
+    const int v = e ? std::atoi(e) : 1;
+    return v >= 0 && v <= 4 ? v : 1;
   }();
   const int shape = c->blk_shape >= 0 ? c->blk_shape : env_shape;
   clg::BlkArgs a = a_in;
@@ -856,7 +868,8 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       cudaMallocHost(&c->sc_host, sizeof(Scalars)) != cudaSuccess ||
       cudaMalloc(&c->flagged, kFlagCap * sizeof(int64_t)) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess) {
+      cudaMalloc(&c->logtab, sizeof(clg::LogTable)) != cudaSuccess ||
+      cudaMalloc(&c->logtab2, sizeof(clg::Log2Table)) != cudaSuccess) {
     clgen_dev_destroy(c);
     return fail(CLGEN_ENOMEM, "clgen_dev_create: allocation failed");
   }
@@ -868,7 +881,13 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
       t.inv_c[i] = static_cast<double>(1.0L / ci);
       t.nlog_inv[i] = static_cast<double>(-logl(static_cast<long double>(t.inv_c[i])));
     }
-    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess) {
+    clg::Log2Table t2;
+    for (int i = 0; i < clg::kLogTable; ++i) {
+      t2.inv_c[i] = t.inv_c[i];
+      t2.nlog2_inv[i] = static_cast<double>(-log2l(static_cast<long double>(t.inv_c[i])));
+    }
+    if (cudaMemcpy(c->logtab, &t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->logtab2, &t2, sizeof t2, cudaMemcpyHostToDevice) != cudaSuccess) {
       clgen_dev_destroy(c);
       return fail(CLGEN_ECUDA, "clgen_dev_create: cannot upload log table");
     }
@@ -886,6 +905,7 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->flagged) cudaFree(c->flagged);
   if (c->logtab) cudaFree(c->logtab);
+  if (c->logtab2) cudaFree(c->logtab2);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   c->counts.release();
   c->offsets.release();
@@ -1356,9 +1376,9 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chun
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (!(class_eps > 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be in (0,1]");
   if (!(chunk_cand == 0.0 || (chunk_cand >= 256.0 && chunk_cand <= 1048576.0)))
-    return fail(CLGEN_EINVAL, "chunk_cand must be 0 (default) or in [256, 2^20]");
+    return fail(CLGEN_EINVAL, "chunk_cand must be 0 (automatic) or in [256, 2^20]");
   c->cls_eps = class_eps;
-  c->chunk_cand = chunk_cand > 0.0 ? chunk_cand : 32768.0;
+  c->chunk_cand = chunk_cand;
   c->cls_valid = c->blk_valid = false;
   c->rng_lo = c->rng_hi = -1;
   return CLGEN_OK;

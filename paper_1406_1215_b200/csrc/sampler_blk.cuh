@@ -50,7 +50,7 @@ constexpr uint32_t kBlkDiag = 1u, kBlkDense = 2u;
 
 struct __align__(16) BlockDesc {
   double pbar;      // RN(RN(w[s_A] w[s_B]) / S): envelope (>= every p_uv of the block)
-  double inv_mu;    // 1 / -log1p(-pbar) (sparse blocks)
+  double inv_mu;    // 1 / -log2(1 - pbar) (sparse blocks)
   double inv_nb;    // RD(1 / nb) (decode_pos)
   int64_t L;        // chunk length in positions
   int64_t nchunks;  // chunks covering [0, na * nb)
@@ -65,6 +65,8 @@ struct BlockRange {
   int64_t c_lo, x_lo, x_hi;
 };
 
+struct Log2Table;
+
 struct BlkArgs {
   const double* __restrict__ w;
   double S;
@@ -75,7 +77,7 @@ struct BlkArgs {
   const int64_t* total_chunks;               // device scalar (written by the scan)
   unsigned long long* queue;
   uint64_t seed_mix;
-  const LogTable* logtab;
+  const Log2Table* logtab;
   // outputs
   int32_t* counts;          // per launch chunk (count mode)
   const int64_t* offsets;   // per launch chunk (write mode)
@@ -96,30 +98,41 @@ struct BlkArgs {
   uint32_t n;
 };
 
-// E = -log(U) ~ Exp(1) by inversion, U = ((x >> 12) + 1/2) 2^-52 in (0,1)
+// E2 = -log2(U) ~ Exp(ln 2) by inversion, U = ((x >> 12) + 1/2) 2^-52 in (0,1)
 // from the top 52 bits of x: y = U 2^52 is built from bits (no int->fp
-// conversion), log y = exponent + table log of the reciprocal centre + a
-// degree-5 log1p series on |t| <= 2^-8; relative error ~2^-47 (statistically
-// exact).  T[i] = {RN(1/c_i), -log RN(1/c_i)}, c_i = 1 + (i + 1/2)/128.
+// conversion), log2 y = exponent + table log2 of the reciprocal centre + a
+// degree-5 log1p series on |t| <= 2^-8 (truncation < 2^-50; statistically
+// exact).  Table entry i = {RN(1/c_i), -log2 RN(1/c_i)}, c_i = 1 + (i + 1/2)/128,
+// replicated 8 times in shared memory (row i = 128 bytes, copy lane & 7) so a
+// 16-byte lookup never meets a bank conflict: the 8 lanes of one LDS.128
+// phase read 8 different bank groups whatever their indices.
+struct Log2Table {
+  double inv_c[kLogTable];
+  double nlog2_inv[kLogTable];
+};
+constexpr int kTabCopies = 8;
+constexpr size_t kTabBytes = static_cast<size_t>(kLogTable) * kTabCopies * sizeof(double2);
+// log2(e) * {1, -1/2, 1/3, -1/4, 1/5}: constant-bank operands of the series FMAs
+__constant__ double kLog2Series[5] = {0x1.71547652b82fep+0, -0x1.71547652b82fep-1, 0x1.ec709dc3a03fdp-2,
+                                      -0x1.71547652b82fep-2, 0x1.2776c50ef9bfep-2};
+
 __device__ __forceinline__ double exp52_y(uint64_t x) {  // (x >> 12) + 1/2, exact
   return __longlong_as_double(static_cast<long long>((x >> 12) | 0x4330000000000000ull)) - (0x1.0p52 - 0.5);
 }
-__device__ __forceinline__ int exp52_index(double y) { return (__double2hiint(y) >> 13) & (kLogTable - 1); }
-__device__ __forceinline__ double exp52_tab(double y, double2 tc) {
+// tab_lane = table base + 16 * (lane & 7) (bytes)
+__device__ __forceinline__ double exp2_52(uint64_t x, const unsigned char* tab_lane) {
+  const double y = exp52_y(x);
   const int yh = __double2hiint(y);
-  const int be = yh >> 20;  // biased exponent (y >= 1/2)
+  const double2 tc = *reinterpret_cast<const double2*>(tab_lane + ((yh >> 6) & ((kLogTable - 1) << 7)));
   const double m = __hiloint2double((yh & 0x000fffff) | 0x3ff00000, __double2loint(y));
   const double t = __fma_rn(m, tc.x, -1.0);
-  double sp = __fma_rn(t, 1.0 / 5.0, -1.0 / 4.0);
-  sp = __fma_rn(t, sp, 1.0 / 3.0);
-  sp = __fma_rn(t, sp, -0.5);
-  sp = __fma_rn(t, sp, 1.0);
-  const double k = __hiloint2double(0x43380000, 1075 - be) - 0x1.8p52;  // 52 - log2 of y's binade, exact
-  return __fma_rn(k, 0x1.62e42fefa39efp-1, __fma_rn(k, 0x1.abc9e3b39803fp-56, -__fma_rn(t, sp, tc.y)));
-}
-__device__ __forceinline__ double exp52(uint64_t x, const double2* __restrict__ T) {
-  const double y = exp52_y(x);
-  return exp52_tab(y, T[exp52_index(y)]);
+  double s = __fma_rn(t, kLog2Series[4], kLog2Series[3]);
+  s = __fma_rn(t, s, kLog2Series[2]);
+  s = __fma_rn(t, s, kLog2Series[1]);
+  s = __fma_rn(t, s, kLog2Series[0]);
+  const double l2m = __fma_rn(t, s, tc.y);                                         // log2 of y's mantissa
+  const double k = __hiloint2double(0x43380000, 1075 - (yh >> 20)) - 0x1.8p52;  // 52 - exponent of y, exact
+  return k - l2m;
 }
 
 __device__ __forceinline__ double unit53(uint64_t b) {  // [0,1)
@@ -138,40 +151,33 @@ __device__ __forceinline__ bool lazy_accept(uint32_t h, double a, uint64_t key, 
   return unit53(r) < s - static_cast<double>(h);  // s - h exact (Sterbenz)
 }
 
-__device__ __forceinline__ double warp_incl_scan_f64(double x) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(CLG_FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
-
-// (row, col) of row-major position x (exact integer double < 2^52) in a
-// block of nb columns.  The quotient is rounded down twice (inv_nb_rd =
-// RD(1/nb), RD product), so it is the true quotient or one less; the exact
-// residual x - row nb in [0, 2 nb) settles it.  No int <-> fp conversions:
-// the integers are read from the low word of 2^52 + value.
-__device__ __forceinline__ void decode_pos(double x, double inv_nb_rd, double nb_d, int32_t nb, uint32_t& row,
-                                           uint32_t& col) {
-  const double qf = __dadd_rd(__dmul_rd(x, inv_nb_rd), 0x1.0p52);  // 2^52 + floor(q)
+// (row, col) of a row-major position in a block of nb columns.  The position
+// travels biased, xb = 2^52 + x (x an integer < 2^52): the low word of xb is
+// x mod 2^32.  floor(x RD(1/nb)) — one FMA rounded down onto the integer
+// grid of [2^52, 2^53) — is the true quotient or one less (x / nb < 2^26, so
+// the 2^-52 relative deficit of RD(1/nb) costs less than one unit); the
+// residual x - row nb in [0, 2 nb) is taken in 32-bit integer arithmetic
+// (nb <= 2^26) and settles it.  No int <-> fp conversions.
+__device__ __forceinline__ void decode_pos(double xb, double inv_nb_rd, uint32_t nb, uint32_t& row, uint32_t& col) {
+  const double qf = __fma_rd(xb - 0x1.0p52, inv_nb_rd, 0x1.0p52);
   uint32_t r = static_cast<uint32_t>(__double2loint(qf));
-  int32_t c = __double2loint(__fma_rn(-(qf - 0x1.0p52), nb_d, x) + 0x1.0p52);
+  uint32_t c = static_cast<uint32_t>(__double2loint(xb)) - r * nb;
   if (c >= nb) {
     c -= nb;
     ++r;
   }
   row = r;
-  col = static_cast<uint32_t>(c);
+  col = c;
 }
 
-constexpr int kStageCap = 512;  // staged pairs per warp (ring / write modes)
-constexpr int kUncCap = 64;     // queued uncertain candidates per warp
+constexpr int kStageCap = 256;  // staged pairs per warp (ring / write modes)
+constexpr int kStageBytes = kStageCap * 8;  // 2048: the per-warp stage is 2048-aligned in shared memory
+constexpr int kUncCap = 64;     // queued uncertain candidates per warp (16-byte records)
+constexpr size_t kWarpQueue = kUncCap * sizeof(uint4) + 16;
 
+// shared memory: [pad to 2048][stage: warps x 2048 B][log2 table copies][per warp: uncertain queue + chunk constants]
 __host__ __device__ inline size_t blk_smem_bytes(int threads) {
-  return kLogTable * sizeof(double2) +
-         static_cast<size_t>(threads / 32) * (kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4) + 16);
+  return kStageBytes + static_cast<size_t>(threads / 32) * (kStageBytes + kWarpQueue) + kTabBytes;
 }
 
 // Per-warp chunk constants needed only on the rare paths (uncertain
@@ -181,21 +187,41 @@ struct WarpChunk {
   double pbar;
 };
 
+__device__ __forceinline__ void sts_pair(uint32_t saddr, uint32_t u, uint32_t v) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr), "r"(u), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint2 lds_pair(uint32_t saddr) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(saddr) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint4 lds_pair2(uint32_t saddr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(saddr) : "memory");
+  return r;
+}
+
 template <int MODE, int E, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* s_log = reinterpret_cast<double2*>(smem_raw);
+  constexpr int NW = THREADS / 32;
   const int wib = threadIdx.x >> 5;
-  unsigned char* wbase = smem_raw + kLogTable * sizeof(double2) +
-                         static_cast<size_t>(wib) * (kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4) + 16);
-  uint2* stage = reinterpret_cast<uint2*>(wbase);
-  uint2* quv = reinterpret_cast<uint2*>(wbase + kStageCap * sizeof(uint2));
-  uint32_t* qh = reinterpret_cast<uint32_t*>(wbase + kStageCap * sizeof(uint2) + kUncCap * sizeof(uint2));
-  WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wbase + kStageCap * sizeof(uint2) + kUncCap * (sizeof(uint2) + 4));
-  for (int i = threadIdx.x; i < kLogTable; i += THREADS) s_log[i] = make_double2(a.logtab->inv_c[i], a.logtab->nlog_inv[i]);
+  // the stage of warp w sits at a 2048-aligned shared address, so a slot's
+  // address is base | (byte counter & 2047): one LOP3
+  unsigned char* sm = smem_raw + ((0u - static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw))) & (kStageBytes - 1));
+  const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + wib * kStageBytes;
+  unsigned char* tab = sm + NW * kStageBytes;
+  unsigned char* wq = tab + kTabBytes + static_cast<size_t>(wib) * kWarpQueue;
+  uint4* quv = reinterpret_cast<uint4*>(wq);  // {u, v, h | id << 11, -}
+  WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wq + kUncCap * sizeof(uint4));
+  for (int i = threadIdx.x; i < kLogTable * kTabCopies; i += THREADS) {
+    const int e = i / kTabCopies;
+    reinterpret_cast<double2*>(tab)[i] = make_double2(a.logtab->inv_c[e], a.logtab->nlog2_inv[e]);
+  }
   __syncthreads();
 
   const int lane = lane_id();
+  const unsigned char* tab_lane = tab + 16 * (lane & (kTabCopies - 1));
   const unsigned lt = lanemask_lt();
   const unsigned long long t_start = a.prof.slots ? globaltimer_ns() : 0ull;
   const int64_t total = *a.total_chunks;
@@ -206,8 +232,8 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   uint2* seg = nullptr;  // null: fold only
   uint32_t smask = 0, wpos = 0;
   if (MODE == kWalkFold && a.ring) {
-    const unsigned nw = gridDim.x * (THREADS >> 5);
-    const unsigned gw = blockIdx.x * (THREADS >> 5) + wib;
+    const unsigned nw = gridDim.x * NW;
+    const unsigned gw = blockIdx.x * NW + wib;
     const int lcap = 63 - __clzll(static_cast<long long>(a.ring_mask + 1ull));
     const int lnw = nw > 1 ? 32 - __clz(nw - 1) : 0;
     int sl = lcap - lnw;
@@ -217,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     seg = a.ring + ((static_cast<unsigned long long>(gw) << sl) & a.ring_mask);
   }
   constexpr bool staging = MODE == kWalkWrite || MODE == kWalkFold;  // fold: every edge is staged (fold + ring at flush)
-  uint32_t head = 0, tail = 0;  // stage counters (warp-uniform)
+  uint32_t head = 0, tail = 0;  // stage counters in BYTES (warp-uniform; 8 per pair)
   uint64_t checksum = 0;
   uint64_t wedges = 0;          // edges of this warp
   int64_t out_pos = 0;          // write mode
@@ -227,11 +253,8 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   auto fold_pair = [&](uint2 e, bool live) {
     checksum += live ? edge_hash(e.x, e.y) : 0ull;
     if (track) {
-      const bool tu = live && (e.x & tmask) == 0, tv = live && (e.y & tmask) == 0;
-      if (__any_sync(CLG_FULL, tu || tv)) {
-        if (tu) atomicAdd(&a.degree[e.x >> a.track_shift], 1u);
-        if (tv) atomicAdd(&a.degree[e.y >> a.track_shift], 1u);
-      }
+      if (live && (e.x & tmask) == 0) atomicAdd(&a.degree[e.x >> a.track_shift], 1u);
+      if (live && (e.y & tmask) == 0) atomicAdd(&a.degree[e.y >> a.track_shift], 1u);
     }
   };
   // flush 64 staged pairs.  Fold mode folds them (2 per lane, every lane
@@ -242,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   auto flush64 = [&]() {
     __syncwarp();
     if (MODE == kWalkFold) {
-      const uint4 v2 = *reinterpret_cast<const uint4*>(&stage[(tail + 2 * lane) & (kStageCap - 1)]);
+      const uint4 v2 = lds_pair2(stage_s | ((tail + 16 * lane) & (kStageBytes - 1)));
       fold_pair(make_uint2(v2.x, v2.y), true);
       fold_pair(make_uint2(v2.z, v2.w), true);
       if (seg) *reinterpret_cast<uint4*>(&seg[(wpos + 2 * lane) & smask]) = v2;
@@ -251,20 +274,20 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
 #pragma unroll
       for (int i = 0; i < 64; i += 32) {
         const int64_t p = out_pos + i + lane;
-        if (p < a.cap) a.pairs[p] = stage[(tail + i + lane) & (kStageCap - 1)];
+        if (p < a.cap) a.pairs[p] = lds_pair(stage_s | ((tail + 8 * (i + lane)) & (kStageBytes - 1)));
         else atomicAdd(a.overflow, 1ull);
       }
       out_pos += 64;
     }
-    tail += 64;
+    tail += 512;
     __syncwarp();
   };
   auto flush_rest = [&]() {  // < 64 left
     __syncwarp();
-    const uint32_t rem = head - tail;
+    const uint32_t rem = (head - tail) >> 3;
     for (uint32_t i0 = 0; i0 < rem; i0 += 32) {
       const bool live = i0 + lane < rem;
-      const uint2 e = stage[(tail + i0 + lane) & (kStageCap - 1)];
+      const uint2 e = lds_pair(stage_s | ((tail + 8 * (i0 + lane)) & (kStageBytes - 1)));
       if (MODE == kWalkFold) {
         fold_pair(e, live);
         if (seg && live) seg[(wpos + i0 + lane) & smask] = e;
@@ -279,17 +302,17 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     tail = head;
     __syncwarp();
   };
-  uint32_t cw = 0;  // edges of the current chunk (warp-uniform)
+  uint32_t cw = 0;  // edges of the current chunk (warp-uniform; staging modes count through head)
   // one candidate slot per lane: stage the accepted pairs
   auto emit1 = [&](bool acc, uint32_t u, uint32_t v) {
     if (MODE == kWalkPairs && acc) atomicAdd(&a.pair_counts[static_cast<uint64_t>(u) * a.n + v], 1u);
     const unsigned b = __ballot_sync(CLG_FULL, acc);
-    const uint32_t nb = __popc(b);
     if (staging) {
-      if (acc) stage[(head + __popc(b & lt)) & (kStageCap - 1)] = make_uint2(u, v);
-      head += nb;
+      if (acc) sts_pair(stage_s | ((head + 8 * __popc(b & lt)) & (kStageBytes - 1)), u, v);
+      head += 8 * __popc(b);
+    } else {
+      cw += __popc(b);
     }
-    cw += nb;
   };
 
   for (;;) {
@@ -312,7 +335,6 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     const int64_t N = static_cast<int64_t>(d.na) * d.nb;
     const int64_t x0 = c * d.L;
     const int64_t x1 = imin64(x0 + d.L, N);
-    const double xend = static_cast<double>(x1);
     // a chunk cut by the launch's source range emits only the rows inside it
     const bool partial = r.x_lo > x0 || r.x_hi < x1;
     const uint64_t key = mix64(seed_mix ^ (static_cast<uint64_t>(b) | (static_cast<uint64_t>(c) << 20)));
@@ -324,12 +346,12 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
     }
     __syncwarp();
     const bool diag = (d.flags & kBlkDiag) != 0;
-    const double nb_d = static_cast<double>(d.nb);
-    const int32_t nbi = static_cast<int32_t>(d.nb);
     uint32_t qn = 0, qt = 0;  // uncertain queue counters (warp-uniform)
     if (MODE == kWalkWrite) out_pos = a.offsets[q];
     cw = 0;
-    const double wlo = static_cast<double>(r.x_lo), whi = static_cast<double>(r.x_hi);
+    const uint32_t head0 = head;
+    // biased window bounds (positions travel as 2^52 + x)
+    const double wlo = static_cast<double>(r.x_lo) + 0x1.0p52, whi = static_cast<double>(r.x_hi) + 0x1.0p52;
 
     // decide the queued uncertain candidates (k <= 32): gather w_u, w_v
     auto resolve = [&](uint32_t k) {
@@ -337,11 +359,10 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       bool acc = false;
       uint32_t u = 0, v = 0;
       if (static_cast<uint32_t>(lane) < k) {
-        const uint32_t i = (qt + lane) & (kUncCap - 1);
-        const uint2 uv = quv[i];
-        const uint32_t hid = qh[i];
-        u = uv.x;
-        v = uv.y;
+        const uint4 rec = quv[(qt + lane) & (kUncCap - 1)];
+        const uint32_t hid = rec.z;
+        u = rec.x;
+        v = rec.y;
         const double q_ = __ddiv_rn(__dmul_rn(a.w[u], a.w[v]), a.S);  // edge_skip.cpp:36
         acc = lazy_accept(hid & 2047u, __ddiv_rn(q_ < 1.0 ? q_ : 1.0, wc.pbar), wc.key, hid >> 11);
       }
@@ -349,57 +370,71 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       __syncwarp();
       emit1(acc, u, v);
       if (staging)
-        while (head - tail >= 64) flush64();
+        while (head - tail >= 512) flush64();
     };
 
     if (!(d.flags & kBlkDense)) {
       // ---- sparse block: each lane runs its own geometric process over its
       // 1/32 of the chunk (memoryless restart at the lane's first position:
-      // no cross-lane dependence), E candidates per iteration ----
-      const double inv_mu = d.inv_mu, inv_nb = d.inv_nb;
-      const uint32_t hs = d.hs;
+      // no cross-lane dependence), E candidates per iteration.  The E gap
+      // draws (RNG, table log2, series) are independent chains issued
+      // together; only the position sum is sequential. ----
+      const double inv_mu2 = d.inv_mu, inv_nb = d.inv_nb;
+      const uint32_t hs = d.hs, nb = d.nb, a0 = d.a0, b0 = d.b0;
       const int64_t ls = (x1 - x0 + 31) >> 5;
       const int64_t lx0 = imin64(x0 + lane * ls, x1);
-      const double lend = static_cast<double>(imin64(lx0 + ls, x1));
-      double pos = static_cast<double>(lx0) - 1.0;  // last candidate position
-      bool live = pos + 1.0 < lend;
-      for (uint32_t id = 0; __any_sync(CLG_FULL, live); id += E) {
+      const double lend = static_cast<double>(imin64(lx0 + ls, x1)) + 0x1.0p52;  // biased end of the lane's positions
+      double pos = static_cast<double>(lx0) + (0x1.0p52 - 1.0);                 // biased last candidate position
+      for (uint32_t id = 0; __any_sync(CLG_FULL, pos < lend); id += E) {
+        double gap[E];
+        uint32_t h[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const uint64_t x = rng.next();
-          // geometric gap floor(E / mu) + 1 (>= 2^52: past every chunk end)
-          pos += __dadd_rd(exp52(x, s_log) * inv_mu, 0x1.0p52) - (0x1.0p52 - 1.0);
-          live = live && pos < lend;
+          h[e] = static_cast<uint32_t>(x) & 2047u;
+          // geometric gap floor(E2 / mu2) + 1 as a double (>= 2^52: past every chunk end)
+          gap[e] = __fma_rd(exp2_52(x, tab_lane), inv_mu2, 0x1.0p52) - (0x1.0p52 - 1.0);
+        }
+        uint32_t u[E], v[E];
+        bool sure[E], unc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          pos += gap[e];
           uint32_t row, col;
-          decode_pos(pos, inv_nb, nb_d, nbi, row, col);
-          bool ok = live && (col > row || !diag);
+          decode_pos(pos, inv_nb, nb, row, col);
+          bool ok = pos < lend && (col > row || !diag);
           if (partial) ok = ok && pos >= wlo && pos < whi;
-          const uint32_t u = d.a0 + row, v = d.b0 + col;
-          const uint32_t h = static_cast<uint32_t>(x) & 2047u;
-          const bool sure = ok && h < hs;
-          emit1(sure, u, v);
-          const bool unc = ok && !sure;
-          const unsigned m = __ballot_sync(CLG_FULL, unc);
+          u[e] = a0 + row;
+          v[e] = b0 + col;
+          sure[e] = ok && h[e] < hs;
+          unc[e] = ok && h[e] >= hs;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          emit1(sure[e], u[e], v[e]);
+          const unsigned m = __ballot_sync(CLG_FULL, unc[e]);
           if (m) {
-            if (unc) {
-              const uint32_t i = (qn + __popc(m & lt)) & (kUncCap - 1);
-              quv[i] = make_uint2(u, v);
-              qh[i] = h | ((((id + e) << 5 | static_cast<uint32_t>(lane)) & 0x1fffffu) << 11);
+            if (unc[e]) {
+              quv[(qn + __popc(m & lt)) & (kUncCap - 1)] =
+                  make_uint4(u[e], v[e], h[e] | ((((id + e) << 5 | static_cast<uint32_t>(lane)) & 0x1fffffu) << 11), 0u);
+              // the weights are read when 32 candidates are queued: start the v miss now
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(a.w + v[e]));
             }
             qn += __popc(m);
             if (qn - qt >= 32) resolve(32);
           }
         }
         if (staging)
-          while (head - tail >= 64) flush64();
+          while (head - tail >= 512) flush64();
       }
     } else {
       // ---- dense block (pbar >= 1): every position is a candidate ----
       const double inv_nb = d.inv_nb;
-      for (double xb = static_cast<double>(x0); xb < xend; xb += 32.0) {
+      const double xend = static_cast<double>(x1) + 0x1.0p52;
+      for (double xb = static_cast<double>(x0) + 0x1.0p52; xb < xend; xb += 32.0) {
         const double x = xb + static_cast<double>(lane);
         uint32_t row, col;
-        decode_pos(x, inv_nb, nb_d, nbi, row, col);
+        decode_pos(x, inv_nb, d.nb, row, col);
         const bool cand = x < xend && (col > row || !diag);
         const uint32_t u = d.a0 + row, v = d.b0 + col;
         bool acc = false;
@@ -412,10 +447,11 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
         }
         emit1(acc, u, v);
         if (staging)
-          while (head - tail >= 64) flush64();
+          while (head - tail >= 512) flush64();
       }
     }
     if (qn != qt) resolve(qn - qt);
+    if (staging) cw = (head - head0) >> 3;
     if (MODE == kWalkCount && lane == 0) a.counts[q] = static_cast<int32_t>(cw);
     wedges += cw;
     if (MODE == kWalkWrite) flush_rest();
@@ -577,7 +613,7 @@ __global__ void blk_desc_kernel(const int64_t* __restrict__ start, const double*
     d.nchunks = (N + L - 1) / L;
     atomicAdd(&plan->dense_blocks, 1);
   } else {
-    d.inv_mu = 1.0 / -log1p(-pbar);
+    d.inv_mu = 0x1.62e42fefa39efp-1 / -log1p(-pbar);  // 1 / -log2(1 - pbar)
     // smallest p_uv of the block, as the generators compute it, over pbar:
     // p_uv / pbar >= that ratio for every pair (monotone FP ops)
     const double qmin = __ddiv_rn(__dmul_rn(wlast[A], wlast[B]), S);
