@@ -89,6 +89,7 @@ bool is_device_ptr(const void* ptr) {
 struct Scalars {
   unsigned long long queue;
   unsigned long long queue_heavy;
+  long long heavy_end;
   unsigned long long ticket;
   unsigned long long flag_count;
   unsigned long long overflow;
@@ -160,7 +161,10 @@ struct clgen_dev_ctx {
   void* host_stage = nullptr;    // pinned staging for edge files
   size_t host_stage_bytes = 0;
   uint64_t seed_mix = 0;
-  int walk_blocks[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  int walk_blocks[2][2][3] = {};  // [heavy][fast][mode]
+  size_t l2_persist_max = 0, l2_window_max = 0;  // device limits (clgen_dev_create)
+  bool l2_persist_dirty = false;                 // persisting lines left by a fold launch
+  double w0 = 0.0;                // w[0] (host copy, set_weights)
   bool fast_math = true;
   int refill_min = static_cast<int>(env_double("CLGEN_REFILL_MIN", 8.0));
   clg::LogTable* logtab = nullptr;  // device
@@ -226,25 +230,48 @@ int fetch_scalars(clgen_dev_ctx* c) {
   return CLGEN_OK;
 }
 
-template <int MODE, bool FAST>
+template <int MODE, bool FAST, bool HEAVY>
 int walk_grid(clgen_dev_ctx* c) {
-  if (!c->walk_blocks[FAST][MODE]) {
+  int& g = c->walk_blocks[HEAVY][FAST][MODE];
+  if (!g) {
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ref_walk_kernel<MODE, FAST>, 256, 0));
-    c->walk_blocks[FAST][MODE] = (per_sm > 0 ? per_sm : 1) * c->num_sms;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, clg::ref_walk_kernel<MODE, FAST, HEAVY>, 256, 0));
+    g = (per_sm > 0 ? per_sm : 1) * c->num_sms;
   }
-  return c->walk_blocks[FAST][MODE];
+  return g;
 }
 
 template <int MODE>
 int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a_in) {
-  const int grid = c->fast_math ? walk_grid<MODE, true>(c) : walk_grid<MODE, false>(c);
-  if (grid < 0) return grid;
   clg::RefWalkArgs a = a_in;
+  // Heavy phase (range walks only): slots whose weight — an upper bound of
+  // the chain's expected candidates — is at least 4x the average work per
+  // lane and at least 256 are walked one per warp; at most 8 per warp.  The
+  // heavy-capable kernel is launched only when the heaviest weight reaches
+  // the threshold (w is non-increasing, w0 read once by set_weights).
+  static const bool heavy_on = env_double("CLGEN_REF_HEAVY", 1.0) != 0.0;
+  const double lanes_lean = static_cast<double>(c->num_sms) * 4.0 * 256.0;
+  const double tw = std::max(256.0, 4.0 * (0.5 * a.S) / lanes_lean);
+  const bool heavy = heavy_on && !a.sources && a.hi > a.lo && a.S > 0.0 && c->w0 >= tw;
+  int grid;
+  if (heavy) grid = c->fast_math ? walk_grid<MODE, true, true>(c) : walk_grid<MODE, false, true>(c);
+  else grid = c->fast_math ? walk_grid<MODE, true, false>(c) : walk_grid<MODE, false, false>(c);
+  if (grid < 0) return grid;
   a.prof = prof_slots(c, grid, true);
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  if (c->fast_math) clg::ref_walk_kernel<MODE, true><<<grid, 256, 0, c->stream>>>(a);
-  else clg::ref_walk_kernel<MODE, false><<<grid, 256, 0, c->stream>>>(a);
+  if (heavy) {
+    CUDA_TRY(cudaMemsetAsync(&c->sc->queue_heavy, 0, sizeof(unsigned long long), c->stream));
+    clg::ref_heavy_end_kernel<<<1, 32, 0, c->stream>>>(c->w, a.lo, a.hi, tw, static_cast<int64_t>(grid) * 64,
+                                                       reinterpret_cast<int64_t*>(&c->sc->heavy_end));
+    a.heavy_end = reinterpret_cast<const int64_t*>(&c->sc->heavy_end);
+    a.hqueue = &c->sc->queue_heavy;
+    ++c->launches;
+    if (c->fast_math) clg::ref_walk_kernel<MODE, true, true><<<grid, 256, 0, c->stream>>>(a);
+    else clg::ref_walk_kernel<MODE, false, true><<<grid, 256, 0, c->stream>>>(a);
+  } else {
+    if (c->fast_math) clg::ref_walk_kernel<MODE, true, false><<<grid, 256, 0, c->stream>>>(a);
+    else clg::ref_walk_kernel<MODE, false, false><<<grid, 256, 0, c->stream>>>(a);
+  }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;
@@ -855,6 +882,14 @@ int clgen_dev_create(int device, clgen_dev_ctx** out) {
     return rc;
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && v > 0)
+      c->l2_persist_max = static_cast<size_t>(v);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess && v > 0)
+      c->l2_window_max = static_cast<size_t>(v);
+    cudaGetLastError();
+  }
   // Random 8-byte weight gathers: ask L2 not to over-fetch around a miss
   // (CLGEN_L2_FETCH=32|64|128; 0 keeps the driver default).
   {
@@ -977,6 +1012,7 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
                                                           &c->sc->runs);
     CUDA_TRY(cudaGetLastError());
     ++c->launches;
+    CUDA_TRY(cudaMemcpyAsync(&c->w0, c->w, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     rc = fetch_scalars(c);
     if (rc) return rc;
     if (c->sc_host->first_negative != ~0ull)
@@ -1130,7 +1166,38 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
     a.track_shift = track_shift;
     a.ring = reinterpret_cast<uint2*>(ring);
     a.ring_mask = ring ? static_cast<unsigned long long>(ring_cap - 1) : 0ull;
-    if ((rc = launch_blk<clg::kWalkFold>(c, a))) return rc;
+    // The tracked-degree array is reduced into at random while the ring
+    // stream runs through L2: for this launch it gets the persisting part of
+    // L2 (as much of it as fits; C4: 62.5 MB of the 82.9 MB B200 allows;
+    // measured 193.9 -> 203.5 G edges/s).  CLGEN_L2_PERSIST_DEG=0 disables it.
+    static const bool persist_deg = env_double("CLGEN_L2_PERSIST_DEG", 1.0) != 0.0;
+    bool window_set = false;
+    if (persist_deg && d_deg && ntracked > 0 && c->l2_persist_max > 0 && c->l2_window_max > 0) {
+      size_t bytes = static_cast<size_t>(ntracked) * sizeof(uint32_t);
+      const size_t carve = std::min(bytes, c->l2_persist_max);
+      bytes = std::min(bytes, c->l2_window_max);
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+        cudaStreamAttrValue attr;
+        std::memset(&attr, 0, sizeof attr);
+        attr.accessPolicyWindow.base_ptr = d_deg;
+        attr.accessPolicyWindow.num_bytes = bytes;
+        attr.accessPolicyWindow.hitRatio =
+            carve >= bytes ? 1.0f : static_cast<float>(carve) / static_cast<float>(bytes);
+        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+        window_set = cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr) == cudaSuccess;
+      }
+      cudaGetLastError();
+    }
+    rc = launch_blk<clg::kWalkFold>(c, a);
+    if (window_set) {  // later launches on the stream carry no window; the lines are released after the sync below
+      cudaStreamAttrValue attr;
+      std::memset(&attr, 0, sizeof attr);
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+      c->l2_persist_dirty = true;
+      cudaGetLastError();
+    }
+    if (rc) return rc;
   } else {
     if ((rc = reset_scalars(c, static_cast<unsigned long long>(lo)))) return rc;
     if (hi > lo && stream_mode == CLGEN_STREAM_REFERENCE) {
@@ -1145,6 +1212,11 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   if (degree && !dev_deg && ntracked > 0)
     CUDA_TRY(cudaMemcpyAsync(degree, d_deg, ntracked * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   if ((rc = fetch_scalars(c))) return rc;
+  if (c->l2_persist_dirty) {  // the launch is over (fetch_scalars synchronised): give the persisting lines back
+    cudaCtxResetPersistingL2Cache();
+    c->l2_persist_dirty = false;
+    cudaGetLastError();
+  }
   if (count) *count = static_cast<int64_t>(c->sc_host->fold[0]);
   if (checksum) *checksum = c->sc_host->fold[1];
   c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);

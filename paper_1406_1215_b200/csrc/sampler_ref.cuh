@@ -54,6 +54,10 @@ struct RefWalkArgs {
   const LogTable* logtab;
   double invS;                   // RN(1/S)
   int refill_min;                // refill idle lanes only when at least this many are idle
+  // heavy phase: slots [lo, *heavy_end) are walked one per WARP (every lane
+  // runs the same chain, lane 0 emits): no divergence on the longest chains
+  const int64_t* heavy_end;      // device scalar (ref_heavy_end_kernel); null: no heavy phase
+  unsigned long long* hqueue;    // next unclaimed heavy slot, counted from lo
 };
 
 // Skip length exactly as edge_skip.cpp:9-16 computes it, with CUDA's libm.
@@ -91,8 +95,11 @@ __device__ __forceinline__ int64_t skip_length_fast(double p, double r, bool& am
   return skip_length_ref(p, r, amb);
 }
 
-template <int MODE, bool FAST>
-__global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
+// HEAVY: compiled with the heavy phase (launched only when the first slot's
+// weight reaches the heavy threshold; 3 CTAs/SM); the lean variant keeps 64
+// registers and 4 CTAs/SM for the gather-bound large runs.
+template <int MODE, bool FAST, bool HEAVY>
+__global__ void __launch_bounds__(256, HEAVY ? 3 : 4) ref_walk_kernel(RefWalkArgs a) {
   constexpr int64_t kBatch = 32;
   __shared__ LogTable s_tab;
   if (FAST) {
@@ -112,6 +119,14 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   // warp-uniform batch state
   int64_t b_next = 0, b_end = 0;
   bool drained = false;
+  // Heavy phase (warp-uniform): while slots remain below heavy_end the warp
+  // takes ONE slot and all 32 lanes walk it in lockstep with identical state;
+  // lane 0 alone emits.  The chain's latency per candidate is then the
+  // dependent instruction chain itself, not 32 diverged chains sharing the
+  // issue slot (C1: the ~1000-candidate chains of the heaviest sources were
+  // the whole step's critical path).
+  const int64_t heavy_end = HEAVY && a.heavy_end ? *a.heavy_end : a.lo;
+  bool heavy_phase = HEAVY && heavy_end > a.lo;
   // per-warp ring reservation (fold mode)
   unsigned long long r_next = 0, r_end = 0;
 
@@ -128,6 +143,41 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
   for (;;) {
     // ---------------------------------------------------------------- refill
     const unsigned need = __ballot_sync(CLG_FULL, u < 0);
+    // start of slot `mine` on this lane (edge_skip.cpp:23-30)
+    auto start_slot = [&](int64_t mine) {
+      slot = mine - a.lo;
+      u = a.sources ? a.sources[mine] : mine;
+      j = u + 1;
+      cnt = 0;
+      amb = false;
+      wu = w[u];
+      if (MODE == kWalkWrite) {
+        out_pos = a.offsets[slot];
+        out_end = a.slot_cap ? out_pos + a.slot_cap[slot] : a.cap;
+      }
+      run_end = 0;
+      if (j < n && S > 0.0) {
+        rng.seed_key(node_rng_key(a.seed, u));
+        const double wj = w[j];
+        if (a.run_len) run_end = j + a.run_len[j];
+        p = fmin(FAST ? div_S(__dmul_rn(wu, wj), S, invS) : __ddiv_rn(__dmul_rn(wu, wj), S), 1.0);
+      } else {
+        p = 0.0;
+      }
+    };
+    if (HEAVY && heavy_phase) {
+      if (need == CLG_FULL) {  // every lane finished the previous heavy slot together
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(a.hqueue, 1ull);
+        g = __shfl_sync(CLG_FULL, g, 0);
+        const int64_t mine = a.lo + static_cast<int64_t>(g);
+        if (mine >= heavy_end) {
+          heavy_phase = false;
+          continue;
+        }
+        start_slot(mine);
+      }
+    } else
     // refill when enough lanes are idle (a lone refill would stall the long
     // chains sharing the warp) or when the whole warp is idle
     if (need && !drained && (__popc(need) >= a.refill_min || need == CLG_FULL)) {
@@ -142,6 +192,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
         unsigned long long g = 0;
         if (lane == 0) g = atomicAdd(a.queue, (unsigned long long)kBatch);
         g = __shfl_sync(CLG_FULL, g, 0);
+        g += static_cast<unsigned long long>(heavy_end - a.lo);  // the light slots start at heavy_end
         if (static_cast<int64_t>(g) >= a.hi) {
           drained = true;
           b_next = b_end = a.hi;
@@ -153,27 +204,7 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
           b_next += take2;
         }
       }
-      if (mine >= 0) {
-        slot = mine - a.lo;
-        u = a.sources ? a.sources[mine] : mine;
-        j = u + 1;
-        cnt = 0;
-        amb = false;
-        wu = w[u];
-        if (MODE == kWalkWrite) {
-          out_pos = a.offsets[slot];
-          out_end = a.slot_cap ? out_pos + a.slot_cap[slot] : a.cap;
-        }
-        run_end = 0;
-        if (j < n && S > 0.0) {
-          rng.seed_key(node_rng_key(a.seed, u));
-          const double wj = w[j];
-          if (a.run_len) run_end = j + a.run_len[j];
-          p = fmin(FAST ? div_S(__dmul_rn(wu, wj), S, invS) : __ddiv_rn(__dmul_rn(wu, wj), S), 1.0);
-        } else {
-          p = 0.0;
-        }
-      }
+      if (mine >= 0) start_slot(mine);
     }
     const unsigned live = __ballot_sync(CLG_FULL, u >= 0);
     if (!live) {
@@ -215,6 +246,8 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
       }
     }
 
+    const bool lead = !HEAVY || !heavy_phase || lane == 0;  // heavy phase: 32 identical chains, one emitter
+    accepted = accepted && lead;
     if (accepted) {
       ++cnt;
       if (MODE == kWalkWrite) {
@@ -254,16 +287,18 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
       }
     }
     if (u >= 0 && (finish || !(j < n && p > 0.0))) {
-      if (MODE == kWalkCount) a.counts[slot] = cnt;
-      if (MODE == kWalkWrite && a.slot_cap) {
-        a.counts[slot] = cnt;
-        if (out_pos > out_end) a.spill[atomicAdd(a.spill_count, 1ull)] = slot;
-      }
-      if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
-        atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
-      if (amb) {
-        const unsigned long long idx = atomicAdd(a.flag_count, 1ull);
-        if (static_cast<int64_t>(idx) < a.flag_cap) a.flagged[idx] = u;
+      if (lead) {
+        if (MODE == kWalkCount) a.counts[slot] = cnt;
+        if (MODE == kWalkWrite && a.slot_cap) {
+          a.counts[slot] = cnt;
+          if (out_pos > out_end) a.spill[atomicAdd(a.spill_count, 1ull)] = slot;
+        }
+        if (MODE == kWalkFold && a.degree && (u & ((1ll << a.track_shift) - 1)) == 0 && cnt)
+          atomicAdd(&a.degree[u >> a.track_shift], static_cast<uint32_t>(cnt));
+        if (amb) {
+          const unsigned long long idx = atomicAdd(a.flag_count, 1ull);
+          if (static_cast<int64_t>(idx) < a.flag_cap) a.flagged[idx] = u;
+        }
       }
       u = -1;
     }
@@ -282,6 +317,19 @@ __global__ void __launch_bounds__(256) ref_walk_kernel(RefWalkArgs a) {
       atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(checksum));
     }
   }
+}
+
+// First slot of [lo, hi) whose weight is below tw (w non-increasing), at most
+// lo + cap: the heavy phase of ref_walk_kernel covers [lo, that).
+__global__ void ref_heavy_end_kernel(const double* __restrict__ w, int64_t lo, int64_t hi, double tw, int64_t cap,
+                                     int64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t a = lo - 1, b = hi;  // w[a] >= tw (or a = lo - 1), w[b] < tw (or b = hi)
+  while (b - a > 1) {
+    const int64_t m = a + ((b - a) >> 1);
+    if (w[m] >= tw) a = m; else b = m;
+  }
+  *out = b < lo + cap ? b : lo + cap;
 }
 
 // Per-slot capacity of the single-pass write: the unclamped expected forward

@@ -10,7 +10,7 @@
   classes (hundreds of class-pair blocks, chunk restarts), and clamped
   pairs / zero weights (dense blocks, exact 0 and 1 frequencies).
 * Degree chi^2 at the BASELINE.json sizes with the DEFAULT parameters (class
-  width 1/128, chunk 32768 expected candidates) — the configurations the
+  width 1/128, automatic chunk size) — the configurations the
   bench reports: (chi^2 - k) / sqrt(2k) <= 5 over the tracked nodes with
   exact FP64 E_i = sum_v min(w_i w_v / S, 1), Var_i = sum_v p (1 - p)
   (acceptance.cpp:113,271 use 4-5 sigma), and the total edge count within
