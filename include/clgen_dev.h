@@ -126,10 +126,13 @@ int clgen_dev_set_fast_math(clgen_dev_ctx* ctx, int enable);
  * and the number of warps. */
 int clgen_dev_set_warp_profile(clgen_dev_ctx* ctx, int enable);
 
-/* Counter-stream kernel shape (no reference counterpart; the edge set does
- * not depend on it): 256 threads x 2 / 3 (default) / 4 / 5 / 6 CTAs per SM
- * for shape 0 / 1 / 2 / 3 / 4, -1 = CLGEN_BLK_SHAPE or the default.  flags must be
- * 0.  Used by the schedule-invariance tests. */
+/* Kernel schedule (no reference counterpart; the edge set does not depend on
+ * it).  shape: counter-stream kernel, 256 threads x 2 / 3 (default) / 4 / 5 /
+ * 6 CTAs per SM for shape 0 / 1 / 2 / 3 / 4, -1 = CLGEN_BLK_SHAPE or the
+ * default.  flags: CLGEN_SHAPE_NO_HEAVY_PHASE walks every reference-stream
+ * slot per lane (by default the heaviest chains are walked one per warp).
+ * Used by the schedule-invariance tests. */
+#define CLGEN_SHAPE_NO_HEAVY_PHASE 1
 int clgen_dev_set_kernel_shape(clgen_dev_ctx* ctx, int shape, int flags);
 int clgen_dev_warp_profile_launches(clgen_dev_ctx* ctx);
 int clgen_dev_warp_profile(clgen_dev_ctx* ctx, int launch, double* max_over_mean, double* mean_ms,

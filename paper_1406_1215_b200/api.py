@@ -147,10 +147,12 @@ class Device:
         reference expressions everywhere; both give identical edges."""
         check(_lib.lib().clgen_dev_set_fast_math(self._h, int(bool(enable))))
 
-    def set_kernel_shape(self, shape: int = -1) -> None:
-        """Counter-stream kernel shape: 256 threads x 2/3/4/5/6 CTAs per SM for
-        shape 0/1/2/3/4 (-1: default 2); the edge set does not depend on it."""
-        check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(shape), 0))
+    def set_kernel_shape(self, shape: int = -1, heavy_phase: bool = True) -> None:
+        """Kernel schedule: counter-stream shape (256 threads x 2/3/4/5/6 CTAs
+        per SM for shape 0/1/2/3/4; -1: default 1) and whether the reference
+        stream walks its heaviest chains one per warp; the edge set does not
+        depend on either."""
+        check(_lib.lib().clgen_dev_set_kernel_shape(self._h, int(shape), 0 if heavy_phase else 1))
 
     def set_warp_profile(self, enable: bool = True) -> None:
         check(_lib.lib().clgen_dev_set_warp_profile(self._h, int(bool(enable))))

@@ -163,6 +163,7 @@ struct clgen_dev_ctx {
   uint64_t seed_mix = 0;
   int walk_blocks[2][2][3] = {};  // [heavy][fast][mode]
   size_t l2_persist_max = 0, l2_window_max = 0;  // device limits (clgen_dev_create)
+  bool ref_heavy = true;                         // clgen_dev_set_kernel_shape flag
   bool l2_persist_dirty = false;                 // persisting lines left by a fold launch
   double w0 = 0.0;                // w[0] (host copy, set_weights)
   bool fast_math = true;
@@ -252,7 +253,7 @@ int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a_in) {
   static const bool heavy_on = env_double("CLGEN_REF_HEAVY", 1.0) != 0.0;
   const double lanes_lean = static_cast<double>(c->num_sms) * 4.0 * 256.0;
   const double tw = std::max(256.0, 4.0 * (0.5 * a.S) / lanes_lean);
-  const bool heavy = heavy_on && !a.sources && a.hi > a.lo && a.S > 0.0 && c->w0 >= tw;
+  const bool heavy = heavy_on && c->ref_heavy && !a.sources && a.hi > a.lo && a.S > 0.0 && c->w0 >= tw;
   int grid;
   if (heavy) grid = c->fast_math ? walk_grid<MODE, true, true>(c) : walk_grid<MODE, false, true>(c);
   else grid = c->fast_math ? walk_grid<MODE, true, false>(c) : walk_grid<MODE, false, false>(c);
@@ -1459,8 +1460,9 @@ int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chun
 int clgen_dev_set_kernel_shape(clgen_dev_ctx* c, int shape, int flags) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (shape < -1 || shape > 4) return fail(CLGEN_EINVAL, "set_kernel_shape: shape must be in [-1, 4]");
-  if (flags != 0) return fail(CLGEN_EINVAL, "set_kernel_shape: flags must be 0");
+  if (flags & ~CLGEN_SHAPE_NO_HEAVY_PHASE) return fail(CLGEN_EINVAL, "set_kernel_shape: unknown flag");
   c->blk_shape = shape;
+  c->ref_heavy = (flags & CLGEN_SHAPE_NO_HEAVY_PHASE) == 0;
   return CLGEN_OK;
 }
 

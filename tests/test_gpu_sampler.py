@@ -173,6 +173,37 @@ def test_fast_math_identical_to_reference_expressions(api, port):
     np.testing.assert_array_equal(api.serial_cl(ws, 1002), exp)
 
 
+def test_heavy_phase_is_schedule_only(api, port):
+    """The reference stream walks its heaviest chains one per warp (every lane
+    on the same chain, lane 0 emitting) before the per-lane phase.  That is a
+    schedule: edges, streamed fold, tracked degrees and flags must not change,
+    on a partial range as well (the heavy prefix is cut by the range)."""
+    cases = [(port.synth_powerlaw(300_000, 2.5, 10.0, 1000.0, 1), 11),   # C1 shape: w >= 256 is heavy
+             (port.synth_powerlaw(200_000, 2.1, 2.0, 1e5, 2), 12),       # saturated heavy head (p = 1 prefix)
+             (np.full(100_000, 50.0), 13)]                               # no heavy slot at all
+    for w, seed in cases:
+        ws = api.make_weight_sequence(w)
+        n = w.size
+        out = {}
+        for heavy in (True, False):
+            ws.device.set_kernel_shape(-1, heavy_phase=heavy)
+            e, nf = api.serial_cl(ws, seed, return_flagged=True)
+            lo, hi = 100, n // 3
+            part = api.create_edges_range(ws, ws.sum_S, lo, hi, seed)
+            st = api.stream_range(ws, ws.sum_S, 0, n, seed, track_shift=2)
+            out[heavy] = (e, nf, part, st.count, st.checksum, st.degree.copy())
+        ws.device.set_kernel_shape(-1)
+        a, b = out[True], out[False]
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[2], b[2])
+        assert a[1] == b[1] and a[3] == b[3] and a[4] == b[4]
+        np.testing.assert_array_equal(a[5], b[5])
+        assert a[3] == len(a[0])
+        if seed == 12:  # and against the oracle where the heavy head is saturated
+            exp, _, _, _ = port.create_edges_range(w, ws.sum_S, 0, n, seed)
+            np.testing.assert_array_equal(a[0], exp)
+
+
 @pytest.mark.parametrize("env", [
     {"CLGEN_REF_SLOT_SIGMA": "0", "CLGEN_REF_SLOT_CONST": "0"},   # most slots spill
     {"CLGEN_REF_SLOT_SIGMA": "1", "CLGEN_REF_SLOT_CONST": "1"},   # some slots spill
