@@ -287,53 +287,69 @@ __global__ void __launch_bounds__(kFoldThreads) fold_tile_fun_kernel(FoldArgs a)
   }
 }
 
-// Phase D: one warp carries the exact running sum across the tiles.
+// Phase D: one warp carries the exact running sum across the tiles.  The
+// tiles' binades and composite maps are loaded 32 at a time (lane l holds tile
+// t0 + l) and handed round by shuffles, so a clean tile costs a few dozen
+// cycles of register work instead of a dependent global load (the walk is
+// sequential by nature: ~2.4e5 tiles at n = 1e9).  Every lane carries the
+// same (s, e, M).
 __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
   const int lane = threadIdx.x;
   int e;
   long long M;
   double s = a.s0;
   binade_of(s, e, M);
-  for (int64_t t = 0; t < T; ++t) {
-    int fast = 0;
-    if (lane == 0) {
-      a.start[t] = s;
-      const int et = a.tbin[t];
-      if (et != kDirty && et == e) {
-        const Fn f = a.tfun[t];
-        const long long M2 = fn_apply(f, M);
+  for (int64_t t0 = 0; t0 < T; t0 += 32) {
+    const int64_t tt = t0 + lane;
+    int et = kDirty;
+    Fn f{0, 0};
+    if (tt < T) {
+      et = a.tbin[tt];
+      f = a.tfun[tt];
+    }
+    double my_start = 0.0;
+    int my_slow = 0;
+    const int cnt = T - t0 < 32 ? static_cast<int>(T - t0) : 32;
+    for (int j = 0; j < cnt; ++j) {
+      const int etj = __shfl_sync(CLG_FULL, et, j);
+      Fn fj;
+      fj.a0 = __shfl_sync(CLG_FULL, f.a0, j);
+      fj.a1 = __shfl_sync(CLG_FULL, f.a1, j);
+      if (lane == j) my_start = s;
+      bool fast = false;
+      if (etj != kDirty && etj == e) {
+        const long long M2 = fn_apply(fj, M);
         if (M2 <= kMaxM) {
           M = M2;
           s = from_binade(e, M);
-          fast = 1;
+          fast = true;
         }
       }
-      a.slow[t] = fast ? 0 : 1;
-    }
-    fast = __shfl_sync(CLG_FULL, fast, 0);
-    if (!fast) {
-      // sequential replay of the tile, 32 elements per chunk
-      s = __shfl_sync(CLG_FULL, s, 0);
-      const int64_t b0 = t * kFoldTile;
-      const int64_t b1 = b0 + kFoldTile < a.m ? b0 + kFoldTile : a.m;
-      for (int64_t c = b0; c < b1; c += 32) {
-        const int64_t k = c + lane;
-        const double xk = k < b1 ? fold_x(a, k) : 0.0;
-        double myout = 0.0;
-        const int cnt = b1 - c < 32 ? static_cast<int>(b1 - c) : 32;
-        for (int j = 0; j < cnt; ++j) {
-          const double xj = __shfl_sync(CLG_FULL, xk, j);
-          const double before = s;
-          s = __dadd_rn(s, xj);
-          if (lane == j) myout = emit_value(a, before, s, xj);
+      if (lane == j) my_slow = fast ? 0 : 1;
+      if (!fast) {
+        // sequential replay of the tile, 32 elements per chunk
+        const int64_t b0 = (t0 + j) * kFoldTile;
+        const int64_t b1 = b0 + kFoldTile < a.m ? b0 + kFoldTile : a.m;
+        for (int64_t c = b0; c < b1; c += 32) {
+          const int64_t k = c + lane;
+          const double xk = k < b1 ? fold_x(a, k) : 0.0;
+          double myout = 0.0;
+          const int n32 = b1 - c < 32 ? static_cast<int>(b1 - c) : 32;
+          for (int i = 0; i < n32; ++i) {
+            const double xi = __shfl_sync(CLG_FULL, xk, i);
+            const double before = s;
+            s = __dadd_rn(s, xi);
+            if (lane == i) myout = emit_value(a, before, s, xi);
+          }
+          if (a.out_mode != kFoldNone && k < b1) fold_put(a, k, myout);
         }
-        if (a.out_mode != kFoldNone && k < b1) fold_put(a, k, myout);
+        binade_of(s, e, M);
       }
-      binade_of(s, e, M);
     }
-    s = __shfl_sync(CLG_FULL, s, 0);
-    M = __shfl_sync(CLG_FULL, M, 0);
-    e = __shfl_sync(CLG_FULL, e, 0);
+    if (tt < T) {
+      a.start[tt] = my_start;
+      a.slow[tt] = my_slow;
+    }
   }
   if (lane == 0) *a.final_out = s;
 }
