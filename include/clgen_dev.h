@@ -108,11 +108,13 @@ int clgen_dev_generate_range(clgen_dev_ctx* ctx, double S, int64_t lo, int64_t h
                              int64_t* n_flagged);
 
 /* Counter-stream tunables: weight-class width (w_first <= (1+class_eps)
- * w_last inside a class; default 1/128, doubled until the classes fit 1024)
- * and the chunk size in expected candidates (0 = automatic: S / 2^19 clamped
- * to [4096, 262144], a function of the weights only; explicit range
- * [256, 2^20]).  Both are part of the stream definition: changing them
- * changes the generated graph (not its law). */
+ * w_last inside a class; 0 = automatic: 1/128, doubled at most twice while the
+ * class-pair blocks would average fewer than 8192 expected candidates; any
+ * width is doubled until the classes fit 1024) and the chunk size in expected
+ * candidates (0 = automatic: S / 2^16 clamped to [4096, 262144]; explicit
+ * range [256, 2^20]).  Automatic values are functions of the weights only.
+ * Both are part of the stream definition: changing them changes the
+ * generated graph (not its law). */
 int clgen_dev_set_counter_params(clgen_dev_ctx* ctx, double class_eps, double chunk_cand);
 /* Reference stream arithmetic: 1 (default) = fast guarded FP64 (table log,
  * series log1p, FMA-certified divisions; falls back to the reference

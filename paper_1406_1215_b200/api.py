@@ -136,10 +136,10 @@ class Device:
         check(_lib.lib().clgen_dev_blocked_sum(self._h, C.byref(out)))
         return out.value
 
-    def set_counter_params(self, class_eps: float = 1.0 / 128, chunk_cand: float = 0.0) -> None:
+    def set_counter_params(self, class_eps: float = 0.0, chunk_cand: float = 0.0) -> None:
         """Counter-stream weight-class width and chunk size in expected
-        candidates (0: default); part of the stream definition (changes the
-        graph, not its law)."""
+        candidates (0: automatic, a function of the weights); part of the
+        stream definition (changes the graph, not its law)."""
         check(_lib.lib().clgen_dev_set_counter_params(self._h, class_eps, chunk_cand))
 
     def set_fast_math(self, enable: bool = True) -> None:

@@ -148,7 +148,8 @@ struct clgen_dev_ctx {
   bool blk_valid = false;
   double blk_S = 0.0;
   int64_t rng_lo = -1, rng_hi = -1;  // launch range the chunk tables hold
-  double cls_eps = env_double("CLGEN_CTR_EPS", 0.0078125);
+  double cls_eps = env_double("CLGEN_CTR_EPS", 0.0);  // 0: automatic (1/128, widened for small graphs)
+  double cls_S = -1.0;                                // S the automatic class table was built for
   double chunk_cand = env_double("CLGEN_CTR_CHUNK", 0.0);  // 0: auto (auto_chunk_cand)
   int blk_shape = -1;  // clgen_dev_set_kernel_shape (-1: CLGEN_BLK_SHAPE / default)
   int blk_grid[4][5] = {};
@@ -467,19 +468,24 @@ int block_boundaries_impl(clgen_dev_ctx* c, int G, int g, double z_offset, doubl
 // Class table of the weights (no host round trip) and block table for S (one
 // synchronisation: the host learns the class and chunk counts to size the
 // per-launch tables); both cached until the weights, S or the parameters change.
-// Automatic chunk size: S / 2 bounds the expected edge count; about 2^18
+// Automatic chunk size: S / 2 bounds the expected edge count; about 2^15
 // chunks per graph, between 4096 candidates (small graphs keep every warp
 // busy) and 262144 (8192 per lane: the lanes of a chunk end within ~2% of
 // one another).  A function of S only, so every GPU count and every cover of
 // the sources cuts the same chunks.
 double auto_chunk_cand(double S) {
-  const double c = std::floor(S * 0x1.0p-19);
+  const double c = std::floor(S * 0x1.0p-16);
   return c < 4096.0 ? 4096.0 : (c > 262144.0 ? 262144.0 : c);
 }
+// Automatic class width: 1/128, doubled (at most twice) while the class-pair
+// blocks would average fewer than this many expected candidates.
+constexpr double kAutoEps = 0.0078125, kAutoMinBlockCand = 8192.0;
 
 int ensure_blocks(clgen_dev_ctx* c, double S) {
   if (c->blk_valid && c->blk_S == S) return CLGEN_OK;
   const int kcap = clg::kClassCap;
+  const bool auto_eps = !(c->cls_eps > 0.0);
+  if (auto_eps && c->cls_S != S) c->cls_valid = false;  // the automatic width looks at S
   if (!c->cls_valid) {
     CUDA_TRY(c->cls_thr.ensure((kcap + 2) * sizeof(double)));
     CUDA_TRY(c->cls_bounds.ensure((kcap + 2) * sizeof(int64_t)));
@@ -489,7 +495,9 @@ int ensure_blocks(clgen_dev_ctx* c, double S) {
     CUDA_TRY(c->cls_plan.ensure(sizeof(clg::ClassPlan)));
     CUDA_TRY(cudaMemsetAsync(c->cls_plan.p, 0, sizeof(clg::ClassPlan), c->stream));
     clg::ClassPlan* dp = c->cls_plan.as<clg::ClassPlan>();
-    clg::cls_grid_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, c->cls_eps, kcap, c->cls_thr.as<double>(), dp);
+    clg::cls_grid_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, auto_eps ? kAutoEps : c->cls_eps,
+                                                 auto_eps ? kAutoMinBlockCand : 0.0, S, kcap, c->cls_thr.as<double>(), dp);
+    c->cls_S = S;
     clg::cls_bounds_kernel<<<(kcap + 256) / 256, 256, 0, c->stream>>>(c->w, c->cls_thr.as<double>(), dp, kcap,
                                                                         c->cls_bounds.as<int64_t>());
     clg::cls_compact_kernel<<<1, 1, 0, c->stream>>>(c->w, c->n, c->cls_bounds.as<int64_t>(), kcap, dp,
@@ -1447,7 +1455,7 @@ int clgen_dev_pair_trials(clgen_dev_ctx* c, double S, uint64_t seed, int64_t tri
 
 int clgen_dev_set_counter_params(clgen_dev_ctx* c, double class_eps, double chunk_cand) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
-  if (!(class_eps > 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be in (0,1]");
+  if (!(class_eps >= 0.0) || !(class_eps <= 1.0)) return fail(CLGEN_EINVAL, "class_eps must be 0 (automatic) or in (0,1]");
   if (!(chunk_cand == 0.0 || (chunk_cand >= 256.0 && chunk_cand <= 1048576.0)))
     return fail(CLGEN_EINVAL, "chunk_cand must be 0 (automatic) or in [256, 2^20]");
   c->cls_eps = class_eps;

@@ -500,9 +500,14 @@ struct ClassPlan {
   int dense_blocks;
 };
 
-// one thread: z, the grid width and the thresholds
-__global__ void cls_grid_kernel(const double* __restrict__ w, int64_t n, double eps0, int kcap, double* thr,
-                                ClassPlan* plan) {
+// one thread: z, the grid width and the thresholds.  min_block_cand > 0
+// (automatic width): starting from eps0 the width is doubled — at most twice
+// for this reason — while the blocks would hold fewer than min_block_cand
+// expected candidates on average (S / 2 over cells^2 / 2): a small graph cut
+// into ~5e5 blocks spends its time on block and chunk set-up, and a chunk
+// cannot be larger than its block.
+__global__ void cls_grid_kernel(const double* __restrict__ w, int64_t n, double eps0, double min_block_cand, double S,
+                                int kcap, double* thr, ClassPlan* plan) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int64_t lo = -1, hi = n;  // first j with w[j] == 0 (w non-negative, non-increasing)
   while (hi - lo > 1) {
@@ -525,10 +530,10 @@ __global__ void cls_grid_kernel(const double* __restrict__ w, int64_t n, double 
   int kg = -1;
   for (int attempt = 0; attempt < 40; ++attempt, eps *= 2.0) {
     const double cells = ceil(log(wmax / wmin) / log1p(eps)) + 1.0;
-    if (cells + zero_class + extra <= kcap) {
-      kg = static_cast<int>(cells);
-      break;
-    }
+    if (cells + zero_class + extra > kcap) continue;
+    if (min_block_cand > 0.0 && attempt < 2 && S / (cells * cells) < min_block_cand) continue;
+    kg = static_cast<int>(cells);
+    break;
   }
   plan->eps = eps;
   if (kg < 0) {

@@ -10,7 +10,7 @@
   classes (hundreds of class-pair blocks, chunk restarts), and clamped
   pairs / zero weights (dense blocks, exact 0 and 1 frequencies).
 * Degree chi^2 at the BASELINE.json sizes with the DEFAULT parameters (class
-  width 1/128, automatic chunk size) — the configurations the
+  automatic class width and chunk size) — the configurations the
   bench reports: (chi^2 - k) / sqrt(2k) <= 5 over the tracked nodes with
   exact FP64 E_i = sum_v min(w_i w_v / S, 1), Var_i = sum_v p (1 - p)
   (acceptance.cpp:113,271 use 4-5 sigma), and the total edge count within
@@ -148,7 +148,7 @@ def test_degree_chi2_full_size_default_params(api, name, shift):
     ws = api.make_weight_sequence(w)
     z, k, zt, res = _chi2_gate(api, ws, w, 2024, shift)
     info = ws.device.counter_plan_info()
-    assert info["class_eps"] <= 1.0 / 64, info  # default width (doubled at most once for the cap)
+    assert info["class_eps"] <= 1.0 / 32, info  # automatic width (1/128, doubled at most twice)
     assert k > 0.9 * w.size
     assert abs(z) <= 5.0, (name, z, k)
     assert abs(zt) <= 4.0, (name, zt)

@@ -93,3 +93,49 @@ def test_torch_distributed_plan_with_device_phases(ref):
         b, reduced, S = out[r]
         assert b == expect, (r, b, expect)
         assert S == rws.sum_S
+
+
+def _nccl_worker(rank, world, port_no, w, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda:0"))
+    from paper_1406_1215_b200 import api, plan, runtime
+    ws = api.make_weight_sequence(w, device=0)
+    dist.barrier()
+    b = plan.plan_ucp_distributed(ws, world, rank)  # the bench's own call: NCCL tensors on the GPU
+    comm = plan.TorchComm(device=runtime.comm_device(0))
+    g = comm.all_gather_f64(ws.sum_S)
+    m = comm.all_reduce_min_i64(np.array([3, 1, 2], np.int64))
+    out[rank] = (b.tolist(), g.tolist(), m.tolist(), dist.get_backend())
+    ws.device.close()
+    dist.destroy_process_group()
+
+
+def test_bench_plan_path_over_nccl_single_rank():
+    """bench.py --gpus N plans through torch.distributed over NCCL with device
+    tensors.  This box has one GPU, so the communicator has one rank: what is
+    pinned here is that the NCCL code path itself (process-group init on the
+    device, barrier, float64 all_gather_into_tensor, int64 MIN all_reduce on
+    GPU tensors) runs and returns the right values."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    import inputs
+    w = inputs.make("c3", 1_000_000)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_no = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_nccl_worker, args=(1, port_no, w, out), nprocs=1, join=True)
+    b, g, m, backend = out[0]
+    assert backend == "nccl"
+    assert b == [0, w.size]
+    assert len(g) == 1 and g[0] > 0.0
+    assert m == [3, 1, 2]
