@@ -60,6 +60,14 @@ int clgen_dev_last_kernel_ms(clgen_dev_ctx* ctx, float* ms);
  * `n` may be 0.  Node ids must fit uint32 (n < 2^32).
  */
 int clgen_dev_set_weights(clgen_dev_ctx* ctx, const double* w, int64_t n);
+/* Starts copying the NEXT weight array (host, ideally page-locked, or device)
+ * into a second device buffer on the context's copy stream and returns at
+ * once: the copy overlaps whatever the context is generating.  The next
+ * clgen_dev_set_weights call with the same pointer and n takes that copy (it
+ * waits for it on the device, swaps the buffers and runs its checks) instead
+ * of copying; any other set_weights call ignores it.  The caller keeps `w`
+ * unchanged until then.  No reference counterpart: ingestion pipelining. */
+int clgen_dev_prefetch_weights(clgen_dev_ctx* ctx, const double* w, int64_t n);
 int64_t clgen_dev_num_nodes(clgen_dev_ctx* ctx);
 /* Device pointer of the context's weight copy (read-only). */
 const double* clgen_dev_weights(clgen_dev_ctx* ctx);

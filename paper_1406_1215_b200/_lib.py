@@ -54,6 +54,7 @@ def _declare(L):
     L.clgen_dev_launch_count.argtypes = [_vp]
     L.clgen_dev_last_kernel_ms.argtypes = [_vp, C.POINTER(C.c_float)]
     L.clgen_dev_set_weights.argtypes = [_vp, _vp, _i64]
+    L.clgen_dev_prefetch_weights.argtypes = [_vp, _vp, _i64]
     L.clgen_dev_num_nodes.restype = _i64
     L.clgen_dev_num_nodes.argtypes = [_vp]
     L.clgen_dev_weights.restype = _vp
@@ -99,7 +100,7 @@ def _declare(L):
 EXPORTS = (
     "clgen_dev_last_error", "clgen_dev_version", "clgen_dev_create", "clgen_dev_destroy",
     "clgen_dev_stream", "clgen_dev_synchronize", "clgen_dev_launch_count",
-    "clgen_dev_last_kernel_ms", "clgen_dev_set_weights", "clgen_dev_num_nodes",
+    "clgen_dev_last_kernel_ms", "clgen_dev_set_weights", "clgen_dev_prefetch_weights", "clgen_dev_num_nodes",
     "clgen_dev_weights", "clgen_dev_blocked_sum", "clgen_dev_blocked_sum_array", "clgen_dev_create_edges_range",
     "clgen_dev_create_edges", "clgen_dev_edge_counts", "clgen_dev_stream_range",
     "clgen_dev_flagged_nodes", "clgen_dev_plan_ucp", "clgen_dev_plan_block_weight",

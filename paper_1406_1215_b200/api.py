@@ -119,6 +119,18 @@ class Device:
         n = int(w.shape[0]) if w is not None else 0
         check(_lib.lib().clgen_dev_set_weights(self._h, _addr(w) if n else None, n))
 
+    def prefetch_weights(self, w) -> None:
+        """Start copying the NEXT weight array on the context's copy stream
+        (overlaps the running generation); the next ``set_weights`` call with
+        the same array takes that copy.  ``w`` must stay unchanged until then."""
+        if isinstance(w, np.ndarray):
+            if w.dtype != np.float64 or not w.flags["C_CONTIGUOUS"]:
+                raise error("prefetch_weights: contiguous float64 array required")
+        elif torch is not None and isinstance(w, torch.Tensor):
+            if w.dtype != torch.float64 or not w.is_contiguous():
+                raise error("prefetch_weights: contiguous float64 tensor required")
+        check(_lib.lib().clgen_dev_prefetch_weights(self._h, _addr(w), int(w.shape[0])))
+
     @property
     def n(self) -> int:
         return int(_lib.lib().clgen_dev_num_nodes(self._h))

@@ -124,6 +124,15 @@ struct clgen_dev_ctx {
   double* w = nullptr;
   int64_t n = 0;
   size_t w_bytes = 0;
+  // clgen_dev_prefetch_weights: the next weight array, copied on its own stream
+  double* w_next = nullptr;
+  size_t w_next_bytes = 0;
+  const double* next_src = nullptr;
+  int64_t next_n = -1;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t next_ready = nullptr;
+  cudaEvent_t swap_done = nullptr;  // main-stream work issued before the last swap (it may read w_next's buffer)
+  bool swapped = false;
   Scalars* sc = nullptr;     // device
   Scalars* sc_host = nullptr;  // pinned mirror
   int64_t* flagged = nullptr;  // device, kFlagCap
@@ -165,6 +174,7 @@ struct clgen_dev_ctx {
   int walk_blocks[2][2][3] = {};  // [heavy][fast][mode]
   size_t l2_persist_max = 0, l2_window_max = 0;  // device limits (clgen_dev_create)
   bool ref_heavy = true;                         // clgen_dev_set_kernel_shape flag
+  size_t l2_carve = 0;                           // persisting carve-out currently set
   bool l2_persist_dirty = false;                 // persisting lines left by a fold launch
   double w0 = 0.0;                // w[0] (host copy, set_weights)
   bool fast_math = true;
@@ -232,6 +242,16 @@ int fetch_scalars(clgen_dev_ctx* c) {
   return CLGEN_OK;
 }
 
+// Persisting L2 lines left by a fold launch (tracked degrees) are given back
+// lazily, when a launch of another kind is about to run (the reset is a
+// device-wide call; a loop of fold launches never pays it).
+void release_persisting_l2(clgen_dev_ctx* c) {
+  if (!c->l2_persist_dirty) return;
+  cudaCtxResetPersistingL2Cache();
+  c->l2_persist_dirty = false;
+  cudaGetLastError();
+}
+
 template <int MODE, bool FAST, bool HEAVY>
 int walk_grid(clgen_dev_ctx* c) {
   int& g = c->walk_blocks[HEAVY][FAST][MODE];
@@ -245,6 +265,7 @@ int walk_grid(clgen_dev_ctx* c) {
 
 template <int MODE>
 int launch_walk(clgen_dev_ctx* c, const clg::RefWalkArgs& a_in) {
+  release_persisting_l2(c);
   clg::RefWalkArgs a = a_in;
   // Heavy phase (range walks only): slots whose weight — an upper bound of
   // the chain's expected candidates — is at least 4x the average work per
@@ -601,6 +622,7 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
     return v >= 0 && v <= 4 ? v : 1;
   }();
   const int shape = c->blk_shape >= 0 ? c->blk_shape : env_shape;
+  if (MODE != clg::kWalkFold) release_persisting_l2(c);
   clg::BlkArgs a = a_in;
   CUDA_TRY(cudaMemsetAsync(&c->sc->queue, 0, sizeof(unsigned long long), c->stream));
   auto launch = [&](auto kern, int threads) -> int {
@@ -945,6 +967,10 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->w) cudaFree(c->w);
+  if (c->w_next) cudaFree(c->w_next);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->next_ready) cudaEventDestroy(c->next_ready);
+  if (c->swap_done) cudaEventDestroy(c->swap_done);
   if (c->sc) cudaFree(c->sc);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->flagged) cudaFree(c->flagged);
@@ -991,6 +1017,37 @@ int clgen_dev_synchronize(clgen_dev_ctx* c) {
   return CLGEN_OK;
 }
 
+int clgen_dev_prefetch_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (n <= 0 || !w) return fail(CLGEN_EINVAL, "prefetch_weights: empty weights");
+  if (n >= (int64_t(1) << 32)) return fail(CLGEN_EINVAL, "set_weights: n exceeds uint32 node ids (n < 2^32)");
+  int rc = set_device(c);
+  if (rc) return rc;
+  if (!c->copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->next_ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->swap_done, cudaEventDisableTiming));
+  }
+  if (c->swapped) CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->swap_done, 0));
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  c->next_n = -1;
+  if (bytes > c->w_next_bytes) {
+    // the previous copy into the old buffer, if any, must be over before it is freed
+    CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+    if (c->w_next) cudaFree(c->w_next);
+    c->w_next = nullptr;
+    c->w_next_bytes = 0;
+    if (cudaMalloc(&c->w_next, bytes) != cudaSuccess)
+      return fail(CLGEN_ENOMEM, "prefetch_weights: cannot allocate %lld weights", (long long)n);
+    c->w_next_bytes = bytes;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->w_next, w, bytes, cudaMemcpyDefault, c->copy_stream));
+  CUDA_TRY(cudaEventRecord(c->next_ready, c->copy_stream));
+  c->next_src = w;
+  c->next_n = n;
+  return CLGEN_OK;
+}
+
 int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
   if (!c) return fail(CLGEN_EINVAL, "null context");
   if (n < 0) return fail(CLGEN_EINVAL, "set_weights: negative n");
@@ -999,6 +1056,17 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
   int rc = set_device(c);
   if (rc) return rc;
   const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  // a copy started by clgen_dev_prefetch_weights for exactly this array: take it
+  const bool prefetched = n > 0 && c->next_n == n && c->next_src == w && c->w_next;
+  if (prefetched) {
+    CUDA_TRY(cudaEventRecord(c->swap_done, c->stream));  // earlier launches may still read the buffer being retired
+    c->swapped = true;
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->next_ready, 0));
+    std::swap(c->w, c->w_next);
+    std::swap(c->w_bytes, c->w_next_bytes);
+  }
+  c->next_n = -1;
+  c->next_src = nullptr;
   if (bytes > c->w_bytes) {
     if (c->w) cudaFree(c->w);
     c->w = nullptr;
@@ -1013,7 +1081,7 @@ int clgen_dev_set_weights(clgen_dev_ctx* c, const double* w, int64_t n) {
   c->rng_lo = c->rng_hi = -1;
   c->plan_G = 0;
   if (n > 0) {
-    CUDA_TRY(cudaMemcpyAsync(c->w, w, bytes, cudaMemcpyDefault, c->stream));
+    if (!prefetched) CUDA_TRY(cudaMemcpyAsync(c->w, w, bytes, cudaMemcpyDefault, c->stream));
     rc = reset_scalars(c, 0);
     if (rc) return rc;
     const int grid = c->num_sms * 8;
@@ -1185,7 +1253,10 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
       size_t bytes = static_cast<size_t>(ntracked) * sizeof(uint32_t);
       const size_t carve = std::min(bytes, c->l2_persist_max);
       bytes = std::min(bytes, c->l2_window_max);
-      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+      // cudaDeviceSetLimit synchronises the device (it would wait for a weight
+      // prefetch in flight): only when the carve-out has to change
+      if (c->l2_carve == carve || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+        c->l2_carve = carve;
         cudaStreamAttrValue attr;
         std::memset(&attr, 0, sizeof attr);
         attr.accessPolicyWindow.base_ptr = d_deg;
@@ -1221,11 +1292,6 @@ int clgen_dev_stream_range(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, u
   if (degree && !dev_deg && ntracked > 0)
     CUDA_TRY(cudaMemcpyAsync(degree, d_deg, ntracked * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   if ((rc = fetch_scalars(c))) return rc;
-  if (c->l2_persist_dirty) {  // the launch is over (fetch_scalars synchronised): give the persisting lines back
-    cudaCtxResetPersistingL2Cache();
-    c->l2_persist_dirty = false;
-    cudaGetLastError();
-  }
   if (count) *count = static_cast<int64_t>(c->sc_host->fold[0]);
   if (checksum) *checksum = c->sc_host->fold[1];
   c->last_flagged = static_cast<int64_t>(c->sc_host->flag_count);

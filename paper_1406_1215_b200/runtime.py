@@ -138,6 +138,10 @@ def e2e_measure(args, w_host: np.ndarray, world: int, rank: int, local: int, lo:
         pinned.numpy()[:] = w_host
     dev = api.Device(local)
     stream = dev.torch_stream()
+    # ingestion pipelining: every step still copies its weights host->device
+    # inside the timed region, but the copy for step k+1 is issued on the
+    # context's copy stream while step k generates (double-buffered weights)
+    pipelined = os.environ.get("CLGEN_E2E_PIPELINE", "1") != "0"
     ring = None
     host_out = None
     deg_host = None
@@ -150,11 +154,13 @@ def e2e_measure(args, w_host: np.ndarray, world: int, rank: int, local: int, lo:
         deg_host = torch.zeros(ntr, dtype=torch.int32, pin_memory=True)
 
     def one():
-        dev.set_weights(pinned)                      # H2D (n * 8 bytes)
+        dev.set_weights(pinned)                      # H2D (n * 8 bytes), or the copy prefetched last step
         S = dev.blocked_sum()
         ws = api.WeightSequence(w_host, S, None, dev)
         b = plan(ws, world, rank)
         a, z = int(b[rank]), int(b[rank + 1])
+        if pipelined:
+            dev.prefetch_weights(pinned)             # next step's H2D, under this step's generation
         if materialise:
             e = api.create_edges_range(ws, S, a, z, seed, out=host_out)  # D2H of the edges
             return int(e.shape[0]), int(e.shape[0]) * 8
@@ -188,4 +194,6 @@ def e2e_measure(args, w_host: np.ndarray, world: int, rank: int, local: int, lo:
     if registered:
         cudart.cudaHostUnregister(w_host.ctypes.data)
     return {"value": e_step / (ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": n * 8,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "h2d": "next step's copy overlapped with this step (clgen_dev_prefetch_weights)" if pipelined
+            else "serial"}

@@ -251,3 +251,45 @@ def test_run_table_bit_exact(api, port, runs, monkeypatch):
                                       err_msg=f"case {t}")
         res = api.stream_range(ws, ws.sum_S, 0, w.size, 40 + t)
         assert (res.count, res.checksum) == (cnt, cks)
+
+
+def test_prefetch_weights_is_plain_ingestion(api, port):
+    """clgen_dev_prefetch_weights only moves the host->device copy of the next
+    weight array off the critical path: generation from the current weights is
+    undisturbed while the copy is in flight, the matching set_weights takes the
+    copy (same edges as a plain set_weights), a non-matching one ignores it,
+    and the contract checks still run on prefetched data."""
+    import torch
+    w1 = port.synth_powerlaw(300_000, 2.5, 10.0, 1000.0, 1)
+    w2 = port.synth_powerlaw(250_000, 2.1, 2.0, 1e4, 2)
+    p1 = torch.from_numpy(w1).pin_memory()
+    p2 = torch.from_numpy(w2).pin_memory()
+    exp1, _, _, _ = port.create_edges_range(w1, port.blocked_sum(w1), 0, w1.size, 5)
+    exp2, _, _, _ = port.create_edges_range(w2, port.blocked_sum(w2), 0, w2.size, 5)
+
+    dev = api.Device(0)
+
+    def edges(w_host):
+        ws = api.WeightSequence(w_host, dev.blocked_sum(), None, dev)
+        return api.serial_cl(ws, 5)
+
+    dev.set_weights(p1)
+    dev.prefetch_weights(p2)                       # in flight while w1 generates
+    np.testing.assert_array_equal(edges(w1), exp1)
+    dev.set_weights(p2)                            # takes the prefetched copy
+    np.testing.assert_array_equal(edges(w2), exp2)
+    dev.prefetch_weights(p1)
+    dev.set_weights(p2)                            # not the prefetched array: plain copy
+    np.testing.assert_array_equal(edges(w2), exp2)
+    for _ in range(3):                             # steady state: both buffers cycle
+        dev.prefetch_weights(p1)
+        dev.set_weights(p1)
+        np.testing.assert_array_equal(edges(w1), exp1)
+        dev.prefetch_weights(p2)
+        dev.set_weights(p2)
+        np.testing.assert_array_equal(edges(w2), exp2)
+    bad = torch.from_numpy(w1[::-1].copy()).pin_memory()
+    dev.prefetch_weights(bad)
+    with pytest.raises(api.error, match="weights unsorted"):
+        dev.set_weights(bad)
+    dev.close()
