@@ -174,10 +174,13 @@ constexpr int kStageCap = 256;  // staged pairs per warp (ring / write modes)
 constexpr int kStageBytes = kStageCap * 8;  // 2048: the per-warp stage is 2048-aligned in shared memory
 constexpr int kUncCap = 64;     // queued uncertain candidates per warp (16-byte records)
 constexpr size_t kWarpQueue = kUncCap * sizeof(uint4) + 16;
+constexpr int kHotDeg = 256;  // tracked counters kept per CTA in shared memory (the heaviest tracked nodes)
 
 // shared memory: [pad to 2048][stage: warps x 2048 B][log2 table copies][per warp: uncertain queue + chunk constants]
+// [hot tracked-degree counters]
 __host__ __device__ inline size_t blk_smem_bytes(int threads) {
-  return kStageBytes + static_cast<size_t>(threads / 32) * (kStageBytes + kWarpQueue) + kTabBytes;
+  return kStageBytes + static_cast<size_t>(threads / 32) * (kStageBytes + kWarpQueue) + kTabBytes +
+         kHotDeg * sizeof(uint32_t);
 }
 
 // Per-warp chunk constants needed only on the rare paths (uncertain
@@ -214,6 +217,13 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   unsigned char* wq = tab + kTabBytes + static_cast<size_t>(wib) * kWarpQueue;
   uint4* quv = reinterpret_cast<uint4*>(wq);  // {u, v, h | id << 11, -}
   WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wq + kUncCap * sizeof(uint4));
+  // The first kHotDeg tracked counters — the heaviest tracked nodes, w being
+  // sorted — are accumulated per CTA in shared memory and added to the global
+  // array once at the end: a hub's row fills whole flushes with one node, and
+  // same-address global reductions serialise in L2 (C3: node 0 alone took 1e5
+  // of them within the 6 ms step).
+  uint32_t* s_hot = reinterpret_cast<uint32_t*>(tab + kTabBytes + static_cast<size_t>(NW) * kWarpQueue);
+  for (int i = threadIdx.x; i < kHotDeg; i += THREADS) s_hot[i] = 0u;
   for (int i = threadIdx.x; i < kLogTable * kTabCopies; i += THREADS) {
     const int e = i / kTabCopies;
     reinterpret_cast<double2*>(tab)[i] = make_double2(a.logtab->inv_c[e], a.logtab->nlog2_inv[e]);
@@ -257,7 +267,15 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   // step, 20% of the step).  The reductions carry an L2 evict_last policy,
   // made on this rare path so no register is held across the hot loop.
   auto red_degree = [&](uint32_t x) {
-    uint32_t* p = &a.degree[x >> a.track_shift];
+    const uint32_t id = x >> a.track_shift;
+    if (id < static_cast<uint32_t>(kHotDeg)) {
+      // address rebuilt from the stage base on this rare path (no register held for it)
+      const uint32_t hot_s = stage_s - (threadIdx.x >> 5) * kStageBytes +
+                             static_cast<uint32_t>(NW * kStageBytes + kTabBytes + NW * kWarpQueue) + 4u * id;
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hot_s) : "memory");
+      return;
+    }
+    uint32_t* p = &a.degree[id];
     asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
                  " red.global.add.L2::cache_hint.u32 [%0], 1, pol;\n}" ::"l"(p) : "memory");
   };
@@ -475,6 +493,11 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       atomicAdd(&a.fold_out[0], static_cast<unsigned long long>(wedges));
       atomicAdd(&a.fold_out[1], static_cast<unsigned long long>(cs));
     }
+  }
+  if (track) {  // every warp of the CTA has left its loop: hand the hot counters over
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHotDeg; i += THREADS)
+      if (s_hot[i]) atomicAdd(&a.degree[i], s_hot[i]);
   }
   if (a.prof.slots && lane == 0) {
     const int g = a.prof.base + static_cast<int>((blockIdx.x * THREADS + threadIdx.x) >> 5);
