@@ -42,6 +42,8 @@
 #include "fastmath.cuh"
 #include "sampler_ref.cuh"
 
+#include <type_traits>
+
 namespace clg {
 
 constexpr int kClassCap = 1024;                 // classes (incl. the zero class)
@@ -414,6 +416,11 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       const int64_t lx0 = imin64(x0 + lane * ls, x1);
       const double lend = static_cast<double>(imin64(lx0 + ls, x1)) + 0x1.0p52;  // biased end of the lane's positions
       double pos = static_cast<double>(lx0) + (0x1.0p52 - 1.0);                 // biased last candidate position
+      // Two instances of the loop: the plain one (off-diagonal block, chunk not
+      // cut by the launch's source range: almost every chunk) drops the
+      // u < v and window tests from every candidate.
+      auto sparse_loop = [&](auto plain_tag) {
+      constexpr bool PLAIN = decltype(plain_tag)::value;
       for (uint32_t id = 0; __any_sync(CLG_FULL, pos < lend); id += E) {
         double gap[E];
         uint32_t h[E];
@@ -431,8 +438,11 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
           pos += gap[e];
           uint32_t row, col;
           decode_pos(pos, inv_nb, nb, row, col);
-          bool ok = pos < lend && (col > row || !diag);
-          if (partial) ok = ok && pos >= wlo && pos < whi;
+          bool ok = pos < lend;
+          if (!PLAIN) {
+            ok = ok && (col > row || !diag);
+            if (partial) ok = ok && pos >= wlo && pos < whi;
+          }
           u[e] = a0 + row;
           v[e] = b0 + col;
           sure[e] = ok && h[e] < hs;
@@ -456,6 +466,9 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
         if (staging)
           while (head - tail >= 512) flush64();
       }
+      };
+      if (!diag && !partial) sparse_loop(std::true_type{});
+      else sparse_loop(std::false_type{});
     } else {
       // ---- dense block (pbar >= 1): every position is a candidate ----
       const double inv_nb = d.inv_nb;
