@@ -287,12 +287,39 @@ __global__ void __launch_bounds__(kFoldThreads) fold_tile_fun_kernel(FoldArgs a)
   }
 }
 
-// Phase D: one warp carries the exact running sum across the tiles.  The
-// tiles' binades and composite maps are loaded 32 at a time (lane l holds tile
-// t0 + l) and handed round by shuffles, so a clean tile costs a few dozen
-// cycles of register work instead of a dependent global load (the walk is
-// sequential by nature: ~2.4e5 tiles at n = 1e9).  Every lane carries the
-// same (s, e, M).
+// Ordered warp-inclusive scan of per-lane maps; returns the lane's EXCLUSIVE
+// prefix, *total = the composition of all 32.
+__device__ __forceinline__ Fn warp_scan_fn(Fn mine, Fn* total) {
+  const int lane = threadIdx.x & 31;
+  Fn inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Fn y;
+    y.a0 = __shfl_up_sync(CLG_FULL, inc.a0, o);
+    y.a1 = __shfl_up_sync(CLG_FULL, inc.a1, o);
+    if (lane >= o) inc = fn_compose(y, inc);
+  }
+  Fn exc;
+  exc.a0 = __shfl_up_sync(CLG_FULL, inc.a0, 1);
+  exc.a1 = __shfl_up_sync(CLG_FULL, inc.a1, 1);
+  if (lane == 0) exc = Fn{0, 0};
+  total->a0 = __shfl_sync(CLG_FULL, inc.a0, 31);
+  total->a1 = __shfl_sync(CLG_FULL, inc.a1, 31);
+  return exc;
+}
+
+// Phase D: one warp carries the exact running sum across the tiles, 32 tiles
+// per step (lane l holds tile t0 + l's binade and composite map).  Every lane
+// carries the same (s, e, M).
+//  * A batch whose 32 tiles are all clean, all in the running sum's binade,
+//    and whose composed map keeps M within the binade is taken in one warp
+//    scan of the maps (x >= 0: M is monotone, so the end check covers every
+//    intermediate value); each lane reads its tile's exact start off its
+//    exclusive prefix.
+//  * Otherwise the tiles are taken one by one; a tile that fails its check is
+//    replayed, and the replay itself goes 32 elements at a time through the
+//    same warp scan of element maps, element by element only for the chunk in
+//    which the sum leaves its binade.
 __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
   const int lane = threadIdx.x;
   int e;
@@ -307,9 +334,21 @@ __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
       et = a.tbin[tt];
       f = a.tfun[tt];
     }
+    const int cnt = T - t0 < 32 ? static_cast<int>(T - t0) : 32;
+    if (cnt == 32 && __all_sync(CLG_FULL, et == e)) {
+      Fn tot;
+      const Fn pre = warp_scan_fn(f, &tot);
+      const long long Mend = fn_apply(tot, M);
+      if (Mend <= kMaxM) {
+        a.start[tt] = from_binade(e, fn_apply(pre, M));
+        a.slow[tt] = 0;
+        M = Mend;
+        s = from_binade(e, M);
+        continue;
+      }
+    }
     double my_start = 0.0;
     int my_slow = 0;
-    const int cnt = T - t0 < 32 ? static_cast<int>(T - t0) : 32;
     for (int j = 0; j < cnt; ++j) {
       const int etj = __shfl_sync(CLG_FULL, et, j);
       Fn fj;
@@ -327,14 +366,29 @@ __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
       }
       if (lane == j) my_slow = fast ? 0 : 1;
       if (!fast) {
-        // sequential replay of the tile, 32 elements per chunk
+        // replay of the tile, 32 elements per chunk
         const int64_t b0 = (t0 + j) * kFoldTile;
         const int64_t b1 = b0 + kFoldTile < a.m ? b0 + kFoldTile : a.m;
         for (int64_t c = b0; c < b1; c += 32) {
           const int64_t k = c + lane;
           const double xk = k < b1 ? fold_x(a, k) : 0.0;
-          double myout = 0.0;
           const int n32 = b1 - c < 32 ? static_cast<int>(b1 - c) : 32;
+          // the chunk as one scan of element maps, when it stays in the binade
+          bool bad = false;
+          const Fn fe = elem_fn(xk, e, bad);
+          Fn tot;
+          const Fn pre = warp_scan_fn(fe, &tot);
+          const long long Mend = fn_apply(tot, M);
+          if (!__any_sync(CLG_FULL, bad) && Mend <= kMaxM) {
+            const long long Mb = fn_apply(pre, M);
+            const double before = from_binade(e, Mb);
+            const double after = from_binade(e, fn_apply(fe, Mb));
+            if (a.out_mode != kFoldNone && k < b1) fold_put(a, k, emit_value(a, before, after, xk));
+            M = Mend;
+            s = from_binade(e, M);
+            continue;
+          }
+          double myout = 0.0;
           for (int i = 0; i < n32; ++i) {
             const double xi = __shfl_sync(CLG_FULL, xk, i);
             const double before = s;
@@ -342,8 +396,8 @@ __global__ void __launch_bounds__(32) fold_spine_kernel(FoldArgs a, int64_t T) {
             if (lane == i) myout = emit_value(a, before, s, xi);
           }
           if (a.out_mode != kFoldNone && k < b1) fold_put(a, k, myout);
+          binade_of(s, e, M);
         }
-        binade_of(s, e, M);
       }
     }
     if (tt < T) {
