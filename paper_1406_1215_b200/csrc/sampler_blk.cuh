@@ -17,7 +17,7 @@
 //    quotients are monotone;
 //  * sparse blocks (pbar < 1): candidates are a Bernoulli(pbar) process over
 //    the block's row-major positions — i.i.d. geometric gaps
-//    floor(E / -log1p(-pbar)) + 1, E ~ Exp(1) — each thinned with probability
+//    floor(E2 / -log2(1-pbar)) + 1, E2 = -log2 U — each thinned with probability
 //    p_uv / pbar.  The class bounds give p_uv / pbar >= hs / 2^11 for the
 //    block's sure threshold hs, so ~98.5% of candidates are accepted from 11
 //    random bits without reading w; the rest gather w_u, w_v (queued per warp
@@ -30,12 +30,13 @@
 //    (chunk, lane).  A launch over sources [lo, hi) claims every chunk whose
 //    rows meet [lo, hi) and emits only those rows, so any cover of the
 //    sources yields the same graph.
-// Per round a warp draws 32 x E gaps (E per lane), places them with one warp
-// prefix sum, decodes (row, col) = (position / nb, position % nb) in exact
-// double arithmetic, and emits accepted pairs through a per-warp shared-memory
-// stage flushed as 16-byte vector stores (ring / fold mode) — the level-2
-// balance is the uniform chunk size: a hub's v-range is spread over as many
-// blocks and chunks as its expected edge count needs.
+// Per iteration every lane draws E gaps for its own 1/32 of the chunk's
+// positions (independent chains: no warp scan, no cross-lane dependence),
+// decodes (row, col) = (position / nb, position % nb) with one FMA rounded
+// down and a 32-bit integer residual, and emits accepted pairs through a
+// per-warp shared-memory stage flushed as 16-byte vector stores (ring / fold
+// mode) — the level-2 balance is the uniform chunk size: a hub's v-range is
+// spread over as many blocks and chunks as its expected edge count needs.
 #pragma once
 
 #include "common.cuh"
