@@ -175,8 +175,9 @@ __device__ __forceinline__ void decode_pos(double xb, double inv_nb_rd, uint32_t
 
 constexpr int kStageCap = 256;  // staged pairs per warp (ring / write modes)
 constexpr int kStageBytes = kStageCap * 8;  // 2048: the per-warp stage is 2048-aligned in shared memory
-constexpr int kUncCap = 64;     // queued uncertain candidates per warp (16-byte records)
-constexpr size_t kWarpQueue = kUncCap * sizeof(uint4) + 16;
+constexpr int kUncCap = 64;     // queued uncertain candidates per warp
+constexpr int kUncRec = 32;     // record: {u, v, h | id << 11, -} + {w_u, w_v} (filled by cp.async)
+constexpr size_t kWarpQueue = kUncCap * kUncRec + 16;
 constexpr int kHotDeg = 256;  // tracked counters kept per CTA in shared memory (the heaviest tracked nodes)
 
 // shared memory: [pad to 2048][stage: warps x 2048 B][log2 table copies][per warp: uncertain queue + chunk constants]
@@ -218,8 +219,7 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
   const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + wib * kStageBytes;
   unsigned char* tab = sm + NW * kStageBytes;
   unsigned char* wq = tab + kTabBytes + static_cast<size_t>(wib) * kWarpQueue;
-  uint4* quv = reinterpret_cast<uint4*>(wq);  // {u, v, h | id << 11, -}
-  WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wq + kUncCap * sizeof(uint4));
+  WarpChunk& wc = *reinterpret_cast<WarpChunk*>(wq + kUncCap * kUncRec);
   // The first kHotDeg tracked counters — the heaviest tracked nodes, w being
   // sorted — are accumulated per CTA in shared memory and added to the global
   // array once at the end: a hub's row fills whole flushes with one node, and
@@ -387,15 +387,18 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
 
     // decide the queued uncertain candidates (k <= 32): gather w_u, w_v
     auto resolve = [&](uint32_t k) {
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this lane's weight copies have landed
       __syncwarp();
       bool acc = false;
       uint32_t u = 0, v = 0;
       if (static_cast<uint32_t>(lane) < k) {
-        const uint4 rec = quv[(qt + lane) & (kUncCap - 1)];
+        const unsigned char* rp = wq + ((qt + lane) & (kUncCap - 1)) * kUncRec;
+        const uint4 rec = *reinterpret_cast<const uint4*>(rp);
+        const double2 ww = *reinterpret_cast<const double2*>(rp + 16);  // w_u, w_v (cp.async, waited for above)
         const uint32_t hid = rec.z;
         u = rec.x;
         v = rec.y;
-        const double q_ = __ddiv_rn(__dmul_rn(a.w[u], a.w[v]), a.S);  // edge_skip.cpp:36
+        const double q_ = __ddiv_rn(__dmul_rn(ww.x, ww.y), a.S);  // edge_skip.cpp:36
         acc = lazy_accept(hid & 2047u, __ddiv_rn(q_ < 1.0 ? q_ : 1.0, wc.pbar), wc.key, hid >> 11);
       }
       qt += k;
@@ -455,10 +458,14 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
           const unsigned m = __ballot_sync(CLG_FULL, unc[e]);
           if (m) {
             if (unc[e]) {
-              quv[(qn + __popc(m & lt)) & (kUncCap - 1)] =
+              unsigned char* rp = wq + ((qn + __popc(m & lt)) & (kUncCap - 1)) * kUncRec;
+              *reinterpret_cast<uint4*>(rp) =
                   make_uint4(u[e], v[e], h[e] | ((((id + e) << 5 | static_cast<uint32_t>(lane)) & 0x1fffffu) << 11), 0u);
-              // the weights are read when 32 candidates are queued: start the v miss now
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(a.w + v[e]));
+              // w_u and w_v travel straight into the record (asynchronous 8-byte
+              // copies, 64-byte L2 fetches): nothing waits until 32 are queued
+              const uint32_t sw = static_cast<uint32_t>(__cvta_generic_to_shared(rp + 16));
+              asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(sw), "l"(a.w + u[e]) : "memory");
+              asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(sw + 8u), "l"(a.w + v[e]) : "memory");
             }
             qn += __popc(m);
             if (qn - qt >= 32) resolve(32);
