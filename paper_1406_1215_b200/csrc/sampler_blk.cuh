@@ -303,10 +303,27 @@ __global__ void __launch_bounds__(THREADS, MINB) blk_kernel(BlkArgs a) {
       if (seg) *reinterpret_cast<uint4*>(&seg[(wpos + 2 * lane) & smask]) = v2;
       wpos += 64;
     } else {
-#pragma unroll
-      for (int i = 0; i < 64; i += 32) {
-        const int64_t p = out_pos + i + lane;
-        if (p < a.cap) a.pairs[p] = lds_pair(stage_s | ((tail + 8 * (i + lane)) & (kStageBytes - 1)));
+      // write mode: the 64 pairs go to pairs[out_pos ..) as 16-byte vector
+      // stores of two pairs.  The burst may start on an odd pair: then pair 0 and
+      // pair 63 are stored alone and lanes 0..30 store pairs (1+2l, 2+2l), so
+      // every vector store stays 16-byte aligned in global memory.
+      const uint32_t odd = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(a.pairs) >> 3) + out_pos) & 1u;  // 16-byte parity of the address
+      const uint32_t k = odd + 2u * lane;  // first staged pair of this lane's vector
+      const int64_t p = out_pos + k;
+      if (k + 1u < 64u) {
+        const uint2 e0 = lds_pair(stage_s | ((tail + 8 * k) & (kStageBytes - 1)));
+        const uint2 e1 = lds_pair(stage_s | ((tail + 8 * (k + 1u)) & (kStageBytes - 1)));
+        if (p + 1 < a.cap) {
+          *reinterpret_cast<uint4*>(&a.pairs[p]) = make_uint4(e0.x, e0.y, e1.x, e1.y);
+        } else {
+          if (p < a.cap) a.pairs[p] = e0;
+          atomicAdd(a.overflow, p < a.cap ? 1ull : 2ull);
+        }
+      }
+      if (odd && (lane == 0 || lane == 31)) {  // the two single pairs of a misaligned burst
+        const uint32_t ks = lane == 0 ? 0u : 63u;
+        const int64_t ps = out_pos + ks;
+        if (ps < a.cap) a.pairs[ps] = lds_pair(stage_s | ((tail + 8 * ks) & (kStageBytes - 1)));
         else atomicAdd(a.overflow, 1ull);
       }
       out_pos += 64;
