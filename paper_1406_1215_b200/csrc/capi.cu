@@ -664,19 +664,23 @@ int launch_blk(clgen_dev_ctx* c, const clg::BlkArgs& a_in) {
   }
 }
 
-__global__ void pairs_to_keys_kernel(const uint2* __restrict__ p, int64_t m, unsigned long long* keys) {
+// Sort keys of the materialised counter stream: (u << bits) | v with bits =
+// ceil(log2 n), so the radix sort runs over 2 * bits key bits (48 at n = 1e7)
+// instead of 64.
+__global__ void pairs_to_keys_kernel(const uint2* __restrict__ p, int64_t m, int bits, unsigned long long* keys) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
     const uint2 e = p[i];
-    keys[i] = (static_cast<unsigned long long>(e.x) << 32) | e.y;
+    keys[i] = (static_cast<unsigned long long>(e.x) << bits) | e.y;
   }
 }
 
-__global__ void keys_to_pairs_kernel(const unsigned long long* __restrict__ keys, int64_t m, uint2* p) {
+__global__ void keys_to_pairs_kernel(const unsigned long long* __restrict__ keys, int64_t m, int bits, uint2* p) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const unsigned long long vmask = (1ull << bits) - 1ull;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
     const unsigned long long k = keys[i];
-    p[i] = make_uint2(static_cast<uint32_t>(k >> 32), static_cast<uint32_t>(k));
+    p[i] = make_uint2(static_cast<uint32_t>(k >> bits), static_cast<uint32_t>(k & vmask));
   }
 }
 
@@ -720,15 +724,18 @@ int materialise_ctr(clgen_dev_ctx* c, double S, int64_t lo, int64_t hi, uint64_t
   a.cap = total;
   if ((rc = launch_blk<clg::kWalkWrite>(c, a))) return rc;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, c->num_sms * 16));
-  pairs_to_keys_kernel<<<grid, 256, 0, c->stream>>>(c->pairs.as<uint2>(), total, c->keys_a.as<unsigned long long>());
+  int bits = 1;
+  while (bits < 32 && (int64_t(1) << bits) < c->n) ++bits;  // node ids < 2^bits
+  pairs_to_keys_kernel<<<grid, 256, 0, c->stream>>>(c->pairs.as<uint2>(), total, bits,
+                                                    c->keys_a.as<unsigned long long>());
   size_t tmp = 0;
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, c->keys_a.as<unsigned long long>(),
-                                          c->keys_b.as<unsigned long long>(), total, 0, 64, c->stream));
+                                          c->keys_b.as<unsigned long long>(), total, 0, 2 * bits, c->stream));
   CUDA_TRY(c->sort_tmp.ensure(tmp > 0 ? tmp : 1));
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(c->sort_tmp.p, tmp, c->keys_a.as<unsigned long long>(),
-                                          c->keys_b.as<unsigned long long>(), total, 0, 64, c->stream));
+                                          c->keys_b.as<unsigned long long>(), total, 0, 2 * bits, c->stream));
   uint2* d_out = is_device_ptr(pairs) ? reinterpret_cast<uint2*>(pairs) : c->pairs.as<uint2>();
-  keys_to_pairs_kernel<<<grid, 256, 0, c->stream>>>(c->keys_b.as<unsigned long long>(), total, d_out);
+  keys_to_pairs_kernel<<<grid, 256, 0, c->stream>>>(c->keys_b.as<unsigned long long>(), total, bits, d_out);
   c->launches += 3;
   CUDA_TRY(cudaGetLastError());
   if (d_out != reinterpret_cast<uint2*>(pairs))
