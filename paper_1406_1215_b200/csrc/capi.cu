@@ -969,6 +969,8 @@ int clgen_dev_destroy(clgen_dev_ctx* c) {
   if (!c) return CLGEN_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);  // a prefetch may still be in flight
+  if (c->l2_persist_dirty) cudaCtxResetPersistingL2Cache();
   if (c->w) cudaFree(c->w);
   if (c->w_next) cudaFree(c->w_next);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
