@@ -73,6 +73,27 @@ int64_t clgen_dev_num_nodes(clgen_dev_ctx* ctx);
 const double* clgen_dev_weights(clgen_dev_ctx* ctx);
 
 /*
+ * Device weight synthesis: replaces synth_powerlaw(n, gamma, w_min, w_max, seed)
+ * (weights.cpp:103-128; continuous truncated power law by inverse CDF over the
+ * sequential synth stream, weights.cpp:17,112) followed, when `sort_desc` is
+ * non-zero, by the descending sort of make_weight_sequence (weights.cpp:32-55;
+ * values only).  `d_out` is DEVICE memory for n doubles; its contents equal the
+ * reference's array bit for bit: the xoshiro stream is entered at every 2048th
+ * draw by GF(2) jump matrices, the inverse CDF's pow is evaluated in
+ * double-double with a rounding certificate, and the draws that cannot be
+ * certified (about 1/16; their count is returned in `n_host_resolved`) are
+ * resolved by the host's libm pow, the reference's own dependency.
+ * `target_mean` > 0 then multiplies every weight by target_mean / (blocked_sum / n)
+ * (the C4 recipe).  Errors like the reference for n < 1, gamma <= 1,
+ * w_min <= 0 or w_min > w_max (CLGEN_EINVAL); CLGEN_ERANGE if the stream holds
+ * a zero draw (probability n * 2^-53), which the reference redraws.
+ * Pass the result to clgen_dev_set_weights (device pointers are accepted).
+ */
+int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double gamma, double w_min, double w_max,
+                             uint64_t seed, int sort_desc, double target_mean, double* d_out,
+                             int64_t* n_host_resolved);
+
+/*
  * S = blocked_sum(w) (weights.cpp:21-30): 4096-element blocks folded left to
  * right from 0.0, partials folded left to right.  Bit-identical.
  */

@@ -264,6 +264,36 @@ def make_weight_sequence(weights, policy: SortPolicy = SortPolicy.require_sorted
     return WeightSequence(w, S, labels, dev)
 
 
+def synth_powerlaw_device(n: int, gamma: float, w_min: float, w_max: float, seed: int,
+                          device: Device | int | None = None, sort: bool = True,
+                          target_mean: float = 0.0):
+    """synth_powerlaw (weights.cpp:103-128) on the device, sorted descending
+    (weights.cpp:32-55) unless ``sort`` is false: a float64 device tensor whose
+    contents equal the reference's array bit for bit, and the number of draws
+    the host's libm had to resolve.  ``target_mean`` > 0 rescales to that mean
+    (the C4 recipe)."""
+    if torch is None:
+        raise RuntimeError("synth_powerlaw_device needs torch for the device buffer")
+    dev = device if isinstance(device, Device) else default_device(device or 0)
+    out = torch.empty(max(int(n), 1), dtype=torch.float64, device=f"cuda:{dev.index}")
+    resolved = C.c_int64()
+    check(_lib.lib().clgen_dev_synth_powerlaw(dev.handle, int(n), float(gamma), float(w_min), float(w_max),
+                                              seed & 0xFFFFFFFFFFFFFFFF, 1 if sort else 0,
+                                              float(target_mean), out.data_ptr(), C.byref(resolved)))
+    return out[: max(int(n), 0)], resolved.value
+
+
+def synth_powerlaw(n: int, gamma: float, w_min: float, w_max: float, seed: int,
+                   device: Device | int | None = None, target_mean: float = 0.0) -> WeightSequence:
+    """make_weight_sequence(synth_powerlaw(...)) with the weights synthesised,
+    sorted and kept on the device (one device-to-host copy for ``.weights``)."""
+    dev = device if isinstance(device, Device) else Device(device or 0)
+    w_dev, _ = synth_powerlaw_device(n, gamma, w_min, w_max, seed, dev, True, target_mean)
+    dev.set_weights(w_dev)
+    w = w_dev.cpu().numpy()
+    return WeightSequence(w, dev.blocked_sum(), np.arange(w.size, dtype=np.int64), dev)
+
+
 def blocked_sum(xs, device: Device | int | None = None) -> float:
     """weights.cpp:21-30 on the device, for any sequence (host or device)."""
     dev = device if isinstance(device, Device) else default_device(device or 0)
