@@ -454,7 +454,8 @@ def run_ours(args):
                        "ring_pairs": None if materialise else (1 << args.ring_log2),
                        "l2": "flushed (256 MB write) between timed steps" if small_inputs
                        else f"inputs larger than L2 ({n * 8 / 1e9:.1f} GB weights)",
-                       "parallelism": f"ucp{world}", "weights_prep_s": round(prep_s, 1)},
+                       "parallelism": f"ucp{world}", "weights_prep_s": round(prep_s, 1),
+                       "weights_prep": ("device (clgen_dev_synth_powerlaw) + read-back" if args.config in runtime.DEVICE_RECIPES and os.environ.get("CLGEN_HOST_SYNTH", "0") != "1" else "host (inputs)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)",

@@ -23,12 +23,28 @@ def comm_device(local: int):
     return torch.device(f"cuda:{local}") if dist.get_backend() == "nccl" else torch.device("cpu")
 
 
+# inputs.make's synth_powerlaw recipes: gamma, w_min, w_max, synth seed, target mean
+DEVICE_RECIPES = {"c3": (2.1, 2.0, 1e5, 1, 0.0), "c4": (2.5, 1.0, 1000.0, 1, 500.0)}
+
+
 def shared_weights(config: str, n: int | None, world: int, rank: int, local: int) -> np.ndarray:
     """Every rank holds all of w.  Rank 0 synthesises the
     workload's weights (input preparation, ``inputs``) into a host file that
     the other ranks map; nothing but a barrier crosses the process group, so
     the only NCCL traffic of a run stays the plan's scalars."""
     import inputs
+    if config in DEVICE_RECIPES and os.environ.get("CLGEN_HOST_SYNTH", "0") != "1":
+        # continuous power-law recipes: every rank synthesises the array on its
+        # own GPU (clgen_dev_synth_powerlaw: bit-identical to inputs.make, which
+        # the CPU reference arm keeps using) and reads it back once
+        import torch
+        gamma, w_min, w_max, seed, mean = DEVICE_RECIPES[config]
+        w_dev, _ = api.synth_powerlaw_device(n or inputs.WORKLOADS[config].n, gamma, w_min, w_max, seed,
+                                             api.default_device(local), True, mean)
+        w = w_dev.cpu().numpy()
+        del w_dev
+        torch.cuda.empty_cache()
+        return w
     if world == 1:
         return inputs.make(config, n)
     import torch.distributed as dist
