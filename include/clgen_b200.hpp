@@ -11,6 +11,7 @@
 //   WeightSequence          weights.hpp:14-20     WeightSequence (+ device context)
 //   make_weight_sequence    weights.hpp:44        make_weight_sequence
 //   blocked_sum             weights.hpp:36        blocked_sum
+//   synth_powerlaw / synth_constant  weights.hpp:47-50   same (synthesised on the device)
 //   expected_total_edges    weights.hpp:55        expected_total_edges (host, O(n))
 //   Edge/EdgeSink/EdgeVector/EdgeCounter  edge_skip.hpp:15-49   same
 //   create_edges            edge_skip.hpp:58-59   create_edges
@@ -115,6 +116,32 @@ inline WeightSequence make_weight_sequence(std::vector<double> weights, SortPoli
   check(clgen_dev_set_weights(ws.device->get(), ws.weights.data(), ws.size()));
   check(clgen_dev_blocked_sum(ws.device->get(), &ws.sum_S));
   return ws;
+}
+
+// weights.cpp:103-128: the array is synthesised and sorted on the device
+// (clgen_dev_synth_powerlaw, bit-identical to the reference's) and read back
+// once for `weights`.  orig_labels is the identity: the synthesiser's draw
+// order is not kept (the reference's labels index its unsorted draws).
+inline WeightSequence synth_powerlaw(node_t n, double gamma, double w_min, double w_max,
+                                     std::uint64_t seed, int device = 0) {
+  WeightSequence ws;
+  ws.device = std::make_shared<Device>(device);
+  check(clgen_dev_synth_powerlaw(ws.device->get(), n, gamma, w_min, w_max, seed, 1, 0.0, nullptr, nullptr));
+  ws.weights.resize(static_cast<size_t>(n));
+  check(clgen_dev_copy_weights(ws.device->get(), ws.weights.data(), n));
+  ws.orig_labels.resize(ws.weights.size());
+  std::iota(ws.orig_labels.begin(), ws.orig_labels.end(), node_t{0});
+  check(clgen_dev_blocked_sum(ws.device->get(), &ws.sum_S));
+  return ws;
+}
+
+// weights.cpp:130-140
+inline WeightSequence synth_constant(node_t n, double d, int device = 0) {
+  if (n < 1) throw error("synth_constant: n must be >= 1");
+  if (d < 0.0) throw error("synth_constant: d must be >= 0");
+  if (d > 0.0 && d >= static_cast<double>(n))
+    throw error("synth_constant: inadmissible (d^2 = " + std::to_string(d * d) + " >= S = " + std::to_string(d * n) + ")");
+  return make_weight_sequence(std::vector<double>(static_cast<size_t>(n), d), SortPolicy::require_sorted, device);
 }
 
 // weights.cpp:21-30 on the device (any sequence)

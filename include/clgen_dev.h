@@ -71,6 +71,10 @@ int clgen_dev_prefetch_weights(clgen_dev_ctx* ctx, const double* w, int64_t n);
 int64_t clgen_dev_num_nodes(clgen_dev_ctx* ctx);
 /* Device pointer of the context's weight copy (read-only). */
 const double* clgen_dev_weights(clgen_dev_ctx* ctx);
+/* CUDA device ordinal of the context. */
+int clgen_dev_device(clgen_dev_ctx* ctx);
+/* Copies the first n resident weights to `out` (host or device memory). */
+int clgen_dev_copy_weights(clgen_dev_ctx* ctx, double* out, int64_t n);
 
 /*
  * Device weight synthesis: replaces synth_powerlaw(n, gamma, w_min, w_max, seed)
@@ -87,7 +91,11 @@ const double* clgen_dev_weights(clgen_dev_ctx* ctx);
  * (the C4 recipe).  Errors like the reference for n < 1, gamma <= 1,
  * w_min <= 0 or w_min > w_max (CLGEN_EINVAL); CLGEN_ERANGE if the stream holds
  * a zero draw (probability n * 2^-53), which the reference redraws.
- * Pass the result to clgen_dev_set_weights (device pointers are accepted).
+ * Pass the result to clgen_dev_set_weights (device pointers are accepted), or
+ * pass d_out = NULL: the array is then synthesised into scratch memory on the
+ * context's device and installed as the context's weights directly
+ * (make_weight_sequence(synth_powerlaw(...)) without a host copy;
+ * clgen_dev_copy_weights reads it back).
  */
 int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double gamma, double w_min, double w_max,
                              uint64_t seed, int sort_desc, double target_mean, double* d_out,

@@ -288,10 +288,24 @@ def synth_powerlaw(n: int, gamma: float, w_min: float, w_max: float, seed: int,
     """make_weight_sequence(synth_powerlaw(...)) with the weights synthesised,
     sorted and kept on the device (one device-to-host copy for ``.weights``)."""
     dev = device if isinstance(device, Device) else Device(device or 0)
-    w_dev, _ = synth_powerlaw_device(n, gamma, w_min, w_max, seed, dev, True, target_mean)
-    dev.set_weights(w_dev)
-    w = w_dev.cpu().numpy()
+    L = _lib.lib()
+    # d_out = NULL: synthesised into scratch and installed as the context's weights
+    check(L.clgen_dev_synth_powerlaw(dev.handle, int(n), float(gamma), float(w_min), float(w_max),
+                                     seed & 0xFFFFFFFFFFFFFFFF, 1, float(target_mean), None, None))
+    w = np.empty(int(n), np.float64)
+    check(L.clgen_dev_copy_weights(dev.handle, w.ctypes.data, int(n)))
     return WeightSequence(w, dev.blocked_sum(), np.arange(w.size, dtype=np.int64), dev)
+
+
+def synth_constant(n: int, d: float, device: Device | int | None = None) -> WeightSequence:
+    """weights.cpp:130-140 (same contract errors)."""
+    if n < 1:
+        raise error("synth_constant: n must be >= 1")
+    if d < 0.0:
+        raise error("synth_constant: d must be >= 0")
+    if d > 0.0 and d >= float(n):
+        raise error(f"synth_constant: inadmissible (d^2 = {d * d:g} >= S = {d * n:g})")
+    return make_weight_sequence(np.full(int(n), float(d)), SortPolicy.require_sorted, device)
 
 
 def blocked_sum(xs, device: Device | int | None = None) -> float:

@@ -1139,6 +1139,18 @@ int64_t clgen_dev_num_nodes(clgen_dev_ctx* c) { return c ? c->n : -1; }
 
 const double* clgen_dev_weights(clgen_dev_ctx* c) { return c ? c->w : nullptr; }
 
+int clgen_dev_device(clgen_dev_ctx* c) { return c ? c->device : -1; }
+
+int clgen_dev_copy_weights(clgen_dev_ctx* c, double* out, int64_t n) {
+  if (!c) return fail(CLGEN_EINVAL, "null context");
+  if (n < 0 || n > c->n || (n > 0 && !out)) return fail(CLGEN_EINVAL, "copy_weights: bad argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  if (n > 0) CUDA_TRY(cudaMemcpyAsync(out, c->w, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDefault, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return CLGEN_OK;
+}
+
 int clgen_dev_blocked_sum(clgen_dev_ctx* c, double* S) {
   if (!c || !S) return fail(CLGEN_EINVAL, "blocked_sum: null argument");
   return blocked_sum_impl(c, c->w, c->n, S);

@@ -293,17 +293,26 @@ extern "C" int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double ga
                                         int64_t* n_host_resolved) {
   if (!ctx) return clgen_internal_fail(CLGEN_EINVAL, "null context");
   // the reference's contract (weights.cpp:105-108)
-  if (n < 1) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: n must be positive");
-  if (!(gamma > 1.0)) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: gamma must exceed 1");
-  if (!(w_min > 0.0) || w_min > w_max) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: need 0 < w_min <= w_max");
+  if (n < 1) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: n must be >= 1");
+  if (!(gamma > 1.0)) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: gamma must be > 1");
+  if (!(w_min > 0.0)) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: w_min must be > 0");
+  if (w_min > w_max) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: w_min > w_max");
   if (n >= (int64_t(1) << 32)) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: n exceeds uint32 node ids (n < 2^32)");
-  if (!d_out) return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: null output");
   cudaPointerAttributes pa{};
-  if (cudaPointerGetAttributes(&pa, d_out) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
-    cudaGetLastError();
-    return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: output must be device memory");
+  Scratch own;  // d_out == NULL: synthesise into scratch and install as the context's weights
+  const bool install = d_out == nullptr;
+  if (install) {
+    pa.device = clgen_dev_device(ctx);
+    SYN_TRY(cudaSetDevice(pa.device));
+    SYN_TRY(own.alloc(sizeof(double) * n));
+    d_out = own.as<double>();
+  } else {
+    if (cudaPointerGetAttributes(&pa, d_out) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return clgen_internal_fail(CLGEN_EINVAL, "synth_powerlaw: output must be device memory");
+    }
+    SYN_TRY(cudaSetDevice(pa.device));
   }
-  SYN_TRY(cudaSetDevice(pa.device));
   cudaStream_t stream = static_cast<cudaStream_t>(clgen_dev_stream(ctx));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pa.device);
@@ -390,5 +399,10 @@ extern "C" int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double ga
   }
   SYN_TRY(cudaStreamSynchronize(stream));
   if (n_host_resolved) *n_host_resolved = resolved;
+  if (install) {
+    const int rc = clgen_dev_set_weights(ctx, d_out, n);
+    if (rc) return rc;
+    SYN_TRY(cudaStreamSynchronize(stream));  // the scratch array is freed on return
+  }
   return CLGEN_OK;
 }

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <vector>
 
+#include <functional>
 #include "clgen_b200.hpp"
 
 namespace clgen = clgen_b200;
@@ -83,6 +84,37 @@ int main() {
     std::int64_t sum = 0;
     for (const auto& r : rep.ranks) sum += r.edges;
     CHECK(sum == rep.total_edges);
+  }
+
+  // synth_powerlaw (weights.cpp:103-128) on the device.  Known answer from the
+  // real reference (tests/golden/edges_pl3000.npz, acceptance.cpp:299 recipe):
+  // synth_powerlaw(3000, 2.5, 2, 50, 0xDE7) generates 6974 edges at seed 1234.
+  {
+    const auto pl = synth_powerlaw(3000, 2.5, 2.0, 50.0, 0xDE7);
+    CHECK(pl.size() == 3000);
+    CHECK(std::is_sorted(pl.weights.begin(), pl.weights.end(), std::greater<double>{}));
+    CHECK(pl.weights.front() <= 50.0 && pl.weights.back() >= 2.0);
+    CHECK(pl.sum_S == blocked_sum(pl.weights));
+    EdgeCounter cnt;
+    CHECK(serial_cl(pl, 1234, cnt) == 6974);
+    const auto same = make_weight_sequence(pl.weights, SortPolicy::require_sorted);
+    CHECK(same.sum_S == pl.sum_S);
+    bool bad = false;
+    try {
+      synth_powerlaw(10, 1.0, 1.0, 2.0, 1);
+    } catch (const error& e) {
+      bad = std::string(e.what()).find("gamma must be > 1") != std::string::npos;
+    }
+    CHECK(bad);
+    const auto k = synth_constant(1000, 5.0);  // weights.cpp:130-140
+    CHECK(k.size() == 1000 && k.sum_S == 5000.0);
+    bad = false;
+    try {
+      synth_constant(4, 4.0);
+    } catch (const error&) {
+      bad = true;
+    }
+    CHECK(bad);
   }
 
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
