@@ -12,6 +12,7 @@
 //   make_weight_sequence    weights.hpp:44        make_weight_sequence
 //   blocked_sum             weights.hpp:36        blocked_sum
 //   synth_powerlaw / synth_constant  weights.hpp:47-50   same (synthesised on the device)
+//   validate / ValidationReport      weights.hpp:22-29,53  same (host)
 //   expected_total_edges    weights.hpp:55        expected_total_edges (host, O(n))
 //   Edge/EdgeSink/EdgeVector/EdgeCounter  edge_skip.hpp:15-49   same
 //   create_edges            edge_skip.hpp:58-59   create_edges
@@ -32,6 +33,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <numeric>
 #include <span>
@@ -142,6 +144,29 @@ inline WeightSequence synth_constant(node_t n, double d, int device = 0) {
   if (d > 0.0 && d >= static_cast<double>(n))
     throw error("synth_constant: inadmissible (d^2 = " + std::to_string(d * d) + " >= S = " + std::to_string(d * n) + ")");
   return make_weight_sequence(std::vector<double>(static_cast<size_t>(n), d), SortPolicy::require_sorted, device);
+}
+
+// weights.hpp:22-29, weights.cpp:142-153 (host: O(n) input statistics)
+struct ValidationReport {
+  bool is_sorted = false;
+  bool admissible = false;  // max w^2 < S; false when S == 0
+  node_t n = 0;
+  double sum_S = 0.0;
+  double max_weight = 0.0;
+  node_t zero_weight_count = 0;
+};
+
+inline ValidationReport validate(const WeightSequence& ws) {
+  ValidationReport rep;
+  rep.n = ws.size();
+  rep.sum_S = ws.sum_S;
+  rep.is_sorted = std::is_sorted(ws.weights.begin(), ws.weights.end(), std::greater<double>{});
+  for (double w : ws.weights) {
+    rep.max_weight = std::max(rep.max_weight, w);
+    if (w == 0.0) ++rep.zero_weight_count;
+  }
+  rep.admissible = ws.sum_S > 0.0 && rep.max_weight * rep.max_weight < ws.sum_S;
+  return rep;
 }
 
 // weights.cpp:21-30 on the device (any sequence)

@@ -308,6 +308,28 @@ def synth_constant(n: int, d: float, device: Device | int | None = None) -> Weig
     return make_weight_sequence(np.full(int(n), float(d)), SortPolicy.require_sorted, device)
 
 
+@dataclass
+class ValidationReport:
+    """weights.hpp:22-29."""
+    is_sorted: bool = False
+    admissible: bool = False  # max w^2 < S; false when S == 0
+    n: int = 0
+    sum_S: float = 0.0
+    max_weight: float = 0.0
+    zero_weight_count: int = 0
+
+
+def validate(ws: WeightSequence) -> ValidationReport:
+    """weights.cpp:142-153 (host: O(n) input statistics)."""
+    w = ws.weights
+    rep = ValidationReport(n=int(w.size), sum_S=float(ws.sum_S))
+    rep.is_sorted = bool(np.all(w[:-1] >= w[1:])) if w.size > 1 else True
+    rep.max_weight = float(max(0.0, w.max())) if w.size else 0.0
+    rep.zero_weight_count = int(np.count_nonzero(w == 0.0))
+    rep.admissible = ws.sum_S > 0.0 and rep.max_weight * rep.max_weight < ws.sum_S
+    return rep
+
+
 def blocked_sum(xs, device: Device | int | None = None) -> float:
     """weights.cpp:21-30 on the device, for any sequence (host or device)."""
     dev = device if isinstance(device, Device) else default_device(device or 0)

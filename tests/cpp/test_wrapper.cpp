@@ -106,6 +106,10 @@ int main() {
       bad = std::string(e.what()).find("gamma must be > 1") != std::string::npos;
     }
     CHECK(bad);
+    const auto vr = validate(pl);  // weights.cpp:142-153
+    CHECK(vr.is_sorted && vr.admissible && vr.n == 3000 && vr.max_weight == pl.weights.front() &&
+          vr.zero_weight_count == 0 && vr.sum_S == pl.sum_S);
+    CHECK(!validate(make_weight_sequence({3, 1, 0}, SortPolicy::require_sorted)).admissible);  // 9 >= 4
     const auto k = synth_constant(1000, 5.0);  // weights.cpp:130-140
     CHECK(k.size() == 1000 && k.sum_S == 5000.0);
     bad = false;
