@@ -330,7 +330,9 @@ extern "C" int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double ga
     Scratch d_mats, d_states, d_idx, d_cnt, d_vals;
     SYN_TRY(d_mats.alloc(sizeof(Mat) * kLevels));
     SYN_TRY(d_states.alloc(sizeof(S256) * chunks));
-    const unsigned long long cap = static_cast<unsigned long long>(n / 8 + 4096);  // ~2x the expected 1/16
+    // ~2x the expected 1/16; weights beyond e^+-60 leave the certificate's range (ddpow.cuh): all may be listed
+    const bool extreme = std::fabs(std::log(w_min)) > 60.0 || std::fabs(std::log(w_max)) > 60.0;
+    const unsigned long long cap = static_cast<unsigned long long>((extreme ? n : n / 8) + 4096);
     SYN_TRY(d_idx.alloc(sizeof(int64_t) * cap));
     SYN_TRY(d_cnt.alloc(2 * sizeof(unsigned long long)));
     SYN_TRY(cudaMemcpyAsync(d_mats.p, mats.data(), sizeof(Mat) * kLevels, cudaMemcpyHostToDevice, stream));
