@@ -102,6 +102,16 @@ int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double gamma, double
                              int64_t* n_host_resolved);
 
 /*
+ * make_weight_sequence(w, SortPolicy::sort_desc) (weights.cpp:32-55) on the
+ * device: sorts the n doubles at `d_w` (DEVICE memory) into non-increasing
+ * order in place, stably, and, when `d_labels` (DEVICE memory, n int64) is
+ * non-NULL, writes orig_labels: labels[i] = input position of the weight now at
+ * i.  Equals the reference's std::stable_sort order, except that a -0.0 sorts
+ * after +0.0 (the reference keeps the two in input order).
+ */
+int clgen_dev_sort_desc(clgen_dev_ctx* ctx, double* d_w, int64_t n, int64_t* d_labels);
+
+/*
  * S = blocked_sum(w) (weights.cpp:21-30): 4096-element blocks folded left to
  * right from 0.0, partials folded left to right.  Bit-identical.
  */

@@ -60,6 +60,7 @@ def _declare(L):
     L.clgen_dev_weights.restype = _vp
     L.clgen_dev_weights.argtypes = [_vp]
     L.clgen_dev_device.argtypes = [_vp]
+    L.clgen_dev_sort_desc.argtypes = [_vp, _vp, _i64, _vp]
     L.clgen_dev_copy_weights.argtypes = [_vp, _vp, _i64]
     L.clgen_dev_blocked_sum.argtypes = [_vp, _dp]
     L.clgen_dev_blocked_sum_array.argtypes = [_vp, _vp, _i64, _dp]
@@ -105,7 +106,7 @@ EXPORTS = (
     "clgen_dev_last_error", "clgen_dev_version", "clgen_dev_create", "clgen_dev_destroy",
     "clgen_dev_stream", "clgen_dev_synchronize", "clgen_dev_launch_count",
     "clgen_dev_last_kernel_ms", "clgen_dev_set_weights", "clgen_dev_prefetch_weights", "clgen_dev_num_nodes",
-    "clgen_dev_weights", "clgen_dev_device", "clgen_dev_copy_weights", "clgen_dev_blocked_sum", "clgen_dev_blocked_sum_array", "clgen_dev_synth_powerlaw", "clgen_dev_create_edges_range",
+    "clgen_dev_weights", "clgen_dev_device", "clgen_dev_copy_weights", "clgen_dev_blocked_sum", "clgen_dev_blocked_sum_array", "clgen_dev_synth_powerlaw", "clgen_dev_sort_desc", "clgen_dev_create_edges_range",
     "clgen_dev_create_edges", "clgen_dev_edge_counts", "clgen_dev_stream_range",
     "clgen_dev_flagged_nodes", "clgen_dev_plan_ucp", "clgen_dev_plan_block_weight",
     "clgen_dev_plan_block_costs", "clgen_dev_plan_block_boundaries", "clgen_dev_generate_range",

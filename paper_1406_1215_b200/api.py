@@ -297,6 +297,18 @@ def synth_powerlaw(n: int, gamma: float, w_min: float, w_max: float, seed: int,
     return WeightSequence(w, dev.blocked_sum(), np.arange(w.size, dtype=np.int64), dev)
 
 
+def sort_desc_device(w, device: Device | int | None = None):
+    """SortPolicy.sort_desc (weights.cpp:32-55) on the device: sorts the float64
+    device tensor ``w`` in place (stable, non-increasing) and returns
+    ``(w, orig_labels)`` with the labels as an int64 device tensor."""
+    if torch is None or not isinstance(w, torch.Tensor) or not w.is_cuda or w.dtype != torch.float64:
+        raise error("sort_desc_device: float64 device tensor required")
+    dev = device if isinstance(device, Device) else default_device(device or w.device.index or 0)
+    labels = torch.empty(w.numel(), dtype=torch.int64, device=w.device)
+    check(_lib.lib().clgen_dev_sort_desc(dev.handle, _addr(w), int(w.numel()), labels.data_ptr()))
+    return w, labels
+
+
 def synth_constant(n: int, d: float, device: Device | int | None = None) -> WeightSequence:
     """weights.cpp:130-140 (same contract errors)."""
     if n < 1:

@@ -247,6 +247,10 @@ __global__ void synth_fill_kernel(double* __restrict__ w, int64_t n, double v) {
     w[i] = v;
 }
 
+__global__ void synth_iota_kernel(int64_t* __restrict__ v, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) v[i] = i;
+}
+
 struct Scratch {
   void* p = nullptr;
   ~Scratch() {
@@ -406,5 +410,49 @@ extern "C" int clgen_dev_synth_powerlaw(clgen_dev_ctx* ctx, int64_t n, double ga
     if (rc) return rc;
     SYN_TRY(cudaStreamSynchronize(stream));  // the scratch array is freed on return
   }
+  return CLGEN_OK;
+}
+
+// make_weight_sequence(w, SortPolicy::sort_desc) (weights.cpp:32-55) on the
+// device: a stable descending sort of the weights carrying each position's
+// original label (LSD radix sort is stable, like the reference's
+// std::stable_sort; a -0.0 sorts after +0.0 here, the reference leaves the two
+// in input order).
+extern "C" int clgen_dev_sort_desc(clgen_dev_ctx* ctx, double* d_w, int64_t n, int64_t* d_labels) {
+  if (!ctx) return clgen_internal_fail(CLGEN_EINVAL, "null context");
+  if (n < 0 || (n > 0 && !d_w)) return clgen_internal_fail(CLGEN_EINVAL, "sort_desc: bad argument");
+  if (n == 0) return CLGEN_OK;
+  cudaPointerAttributes pa{}, pl{};
+  if (cudaPointerGetAttributes(&pa, d_w) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+      (d_labels && (cudaPointerGetAttributes(&pl, d_labels) != cudaSuccess || pl.type != cudaMemoryTypeDevice))) {
+    cudaGetLastError();
+    return clgen_internal_fail(CLGEN_EINVAL, "sort_desc: weights and labels must be device memory");
+  }
+  SYN_TRY(cudaSetDevice(pa.device));
+  cudaStream_t stream = static_cast<cudaStream_t>(clgen_dev_stream(ctx));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pa.device);
+  Scratch alt_w, alt_l, tmp;
+  SYN_TRY(alt_w.alloc(sizeof(double) * n));
+  cub::DoubleBuffer<double> keys(d_w, alt_w.as<double>());
+  size_t tmp_bytes = 0;
+  if (d_labels) {
+    SYN_TRY(alt_l.alloc(sizeof(int64_t) * n));
+    synth_iota_kernel<<<sms * 8, 256, 0, stream>>>(d_labels, n);
+    SYN_TRY(cudaGetLastError());
+    cub::DoubleBuffer<int64_t> vals(d_labels, alt_l.as<int64_t>());
+    SYN_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, keys, vals, n, 0, 64, stream));
+    SYN_TRY(tmp.alloc(tmp_bytes));
+    SYN_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, keys, vals, n, 0, 64, stream));
+    if (vals.Current() != d_labels)
+      SYN_TRY(cudaMemcpyAsync(d_labels, vals.Current(), sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, stream));
+  } else {
+    SYN_TRY(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp_bytes, keys, n, 0, 64, stream));
+    SYN_TRY(tmp.alloc(tmp_bytes));
+    SYN_TRY(cub::DeviceRadixSort::SortKeysDescending(tmp.p, tmp_bytes, keys, n, 0, 64, stream));
+  }
+  if (keys.Current() != d_w)
+    SYN_TRY(cudaMemcpyAsync(d_w, keys.Current(), sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+  SYN_TRY(cudaStreamSynchronize(stream));
   return CLGEN_OK;
 }
